@@ -1,0 +1,600 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU ORACLE for the skew-symmetric
+ * eigensolver of Penke et al., arXiv 1912.04062.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load this library.  It shares no code,
+ * header, table or helper with the CUDA path (paper_1912_04062_b200/), and the
+ * CUDA path never calls it.
+ *
+ * Everything is FP64, column-major, 0-based.  A skew matrix is given by its
+ * strictly lower triangle ("A = -A^T"); the diagonal
+ * and upper triangle are never read.
+ *
+ * Route (Algorithm 1, with the ONE-STEP reduction of
+ * Section 2.3.1, unblocked):
+ *   O1/O2  orc_tridiagonalize     Householder tridiagonalisation, one reflector per
+ *                                 column, skew rank-2 update  A <- A + v w^T - w v^T
+ *                                 (Eqs. (2)-(5) with u1 = -u2)
+ *   O3/O4  orc_bisect             Sturm-count bisection on T_sym = tridiag(alpha,0,alpha)
+ *                                 (Lemma 1; "bisection")
+ *   O5/O6  orc_inverse_iteration  inverse iteration + reorthogonalisation
+ *   O7     orc_apply_D            Q <- D Q_diag, D = diag(i^k)  (Alg. 1 step 3)
+ *   O8     orc_backtransform      Q <- Q_trd Q on Re and Im planes independently
+ *                                 (Alg. 1 step 4)
+ *   O0     orc_cholesky/orc_form_W  BSE steps 2-3
+ * Readings of the paper: R1 D = diag(i^0..i^{n-1});
+ * R2 alpha_k = A_trd[k,k+1] = -A_trd[k+1,k]; R3 LAPACK dlarfg sign convention;
+ * R4 the 0.5 tau^2 v^T A v term of Eq. (3) is identically 0 for skew A and is dropped;
+ * R5 positive half, descending; R9 dstebz/dstein-like bisection + inverse iteration.
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_*.py against
+ * closed forms, invariants, worked examples, library routines or brute force
+ * (DESIGN.md "Oracle pins"); none is "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <float.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define IDX(i, j, ld) ((size_t)(i) + (size_t)(j) * (size_t)(ld))
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* ------------------------------------------------------------------------- */
+/* Householder reflector, LAPACK dlarfg convention (reading R3).
+ * Given x (length m >= 1) returns v (v[0] = 1), tau, beta with
+ * (I - tau v v^T) x = beta e1.  beta = -sign(x0) ||x|| with sign(0) = +;
+ * if ||x[1:]|| = 0 then tau = 0, beta = x0, v = e1.
+ * PAPER.md:239-242 ("a reflection onto a scaled first unit vector").          */
+void orc_householder(int64_t m, const double* x, double* v, double* tau, double* beta) {
+  double x0 = x[0];
+  double s = 0.0;
+  for (int64_t i = 1; i < m; i++) s += x[i] * x[i];
+  v[0] = 1.0;
+  if (s == 0.0) {
+    *tau = 0.0;
+    *beta = x0;
+    for (int64_t i = 1; i < m; i++) v[i] = 0.0;
+    return;
+  }
+  double nrm = sqrt(x0 * x0 + s);
+  double b = (x0 >= 0.0) ? -nrm : nrm;
+  *tau = (b - x0) / b;
+  double scal = 1.0 / (x0 - b);
+  for (int64_t i = 1; i < m; i++) v[i] = x[i] * scal;
+  *beta = b;
+}
+
+/* Skew matrix-vector product from the strictly lower triangle (skew-SYMV,
+ * PAPER.md:459-462): y = A x with A = L - L^T.               */
+void orc_skew_matvec(int64_t n, const double* A, int64_t lda, const double* x, double* y) {
+  for (int64_t p = 0; p < n; p++) y[p] = 0.0;
+  for (int64_t q = 0; q < n; q++)
+    for (int64_t p = q + 1; p < n; p++) {
+      double a = A[IDX(p, q, lda)];
+      y[p] += a * x[q];   /* a_pq x_q         */
+      y[q] -= a * x[p];   /* a_qp = -a_pq     */
+    }
+}
+
+/* Skew rank-2 update A <- A - v u^T + u v^T on the strictly lower triangle
+ * (skew-SYR2).                                           */
+void orc_skew_rank2(int64_t n, double* A, int64_t lda, const double* u, const double* v) {
+  for (int64_t q = 0; q < n; q++)
+    for (int64_t p = q + 1; p < n; p++)
+      A[IDX(p, q, lda)] += -v[p] * u[q] + u[p] * v[q];
+}
+
+/* ------------------------------------------------------------------------- */
+/* O1/O2: one-step Householder tridiagonalisation.
+ * A (n x n, lda) : strictly lower triangle in; on return A[j+2:n, j] holds v_j[1:]
+ *                  (v_j[0] = 1 implicit at row j+1).
+ * tau (n-1)      : tau_j (tau_{n-2} = 0).
+ * alpha (n-1)    : Lemma-1 off-diagonals, alpha_k = -A_trd[k+1,k]  (reading R2).
+ * For each column j:  x = A[j+1:n, j];  (v, tau, beta) = householder(x);
+ *   w = tau * S v  with S = A[j+1:, j+1:] skew (no 0.5 tau^2 v^T S v term: it is 0
+ *   for skew S, reading R4);  S <- S + v w^T - w v^T   (Eq. (5) with u1 = -u2 = -w,
+ *   PAPER.md:392-399).                                                        */
+void orc_tridiagonalize(int64_t n, double* A, int64_t lda, double* alpha, double* tau) {
+  if (n < 2) return;
+  double* v = (double*)malloc(sizeof(double) * (size_t)n);
+  double* w = (double*)malloc(sizeof(double) * (size_t)n);
+  double* sub = (double*)malloc(sizeof(double) * (size_t)n);
+  for (int64_t j = 0; j + 2 < n; j++) {
+    int64_t m = n - j - 1;              /* trailing block rows j+1 .. n-1 */
+    double* x = &A[IDX(j + 1, j, lda)];
+    double t, beta;
+    orc_householder(m, x, v, &t, &beta);
+    sub[j] = beta;
+    tau[j] = t;
+    x[0] = beta;
+    for (int64_t i = 1; i < m; i++) x[i] = v[i];   /* store v in place */
+    if (t == 0.0) continue;
+    /* w = tau * S v, S = A[j+1:n, j+1:n] from its lower triangle.  Local index
+     * p, q in [0, m): S_pq = A[j+1+p, j+1+q] for p > q, S_pq = -S_qp for p < q. */
+    const int64_t o = j + 1;
+#pragma omp parallel
+    {
+#ifdef _OPENMP
+      int nt = omp_get_num_threads(), id = omp_get_thread_num();
+#else
+      int nt = 1, id = 0;
+#endif
+      int64_t r0 = m * id / nt, r1 = m * (id + 1) / nt;
+      for (int64_t p = r0; p < r1; p++) w[p] = 0.0;
+      /* sum_{q<p} S_pq v_q, accumulated column by column over this thread's rows */
+      for (int64_t q = 0; q < r1; q++) {
+        const double* col = &A[IDX(o, o + q, lda)];
+        double vq = v[q];
+        for (int64_t p = (q + 1 > r0 ? q + 1 : r0); p < r1; p++) w[p] += col[p] * vq;
+      }
+      /* - sum_{q>p} S_qp v_q  (column p below the diagonal) */
+      for (int64_t p = r0; p < r1; p++) {
+        const double* col = &A[IDX(o, o + p, lda)];
+        double s = 0.0;
+        for (int64_t q = p + 1; q < m; q++) s += col[q] * v[q];
+        w[p] = t * (w[p] - s);
+      }
+    }
+    /* S_pq += v_p w_q - w_p v_q  for p > q */
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t q = 0; q < m; q++) {
+      double* col = &A[IDX(o, o + q, lda)];
+      double wq = w[q], vq = v[q];
+      for (int64_t p = q + 1; p < m; p++) col[p] += v[p] * wq - w[p] * vq;
+    }
+  }
+  if (n >= 2) {
+    sub[n - 2] = A[IDX(n - 1, n - 2, lda)];
+    tau[n - 2] = 0.0;
+  }
+  for (int64_t k = 0; k + 1 < n; k++) alpha[k] = -sub[k];
+  free(v); free(w); free(sub);
+}
+
+/* ------------------------------------------------------------------------- */
+/* O3/O4: Sturm count and bisection on T_sym = tridiag(alpha, 0, alpha)
+ * (Lemma 1; Algorithm 1 step 2, PAPER.md:288-305;
+ * "bisection").  Count N(sigma) = #{eigenvalues < sigma} from
+ * the LDL^T pivots q_0 = -sigma, q_k = -sigma - alpha_{k-1}^2 / q_{k-1}
+ * (|q| < pivmin replaced by -pivmin, as LAPACK dstebz).                      */
+int64_t orc_sturm_count(int64_t n, const double* alpha, double sigma, double pivmin) {
+  int64_t cnt = 0;
+  double q = -sigma;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0) cnt++;
+  for (int64_t k = 1; k < n; k++) {
+    q = -sigma - alpha[k - 1] * alpha[k - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0) cnt++;
+  }
+  return cnt;
+}
+
+static double orc_pivmin(int64_t n, const double* alpha) {
+  double mx = 1.0;
+  for (int64_t k = 0; k + 1 < n; k++) if (alpha[k] * alpha[k] > mx) mx = alpha[k] * alpha[k];
+  return DBL_MIN * mx;
+}
+
+/* Gershgorin bound g = max_k (|alpha_{k-1}| + |alpha_k|) of T_sym. */
+double orc_gershgorin(int64_t n, const double* alpha) {
+  double g = 0.0;
+  for (int64_t k = 0; k < n; k++) {
+    double r = (k > 0 ? fabs(alpha[k - 1]) : 0.0) + (k + 1 < n ? fabs(alpha[k]) : 0.0);
+    if (r > g) g = r;
+  }
+  return g;
+}
+
+/* Eigenvalue with 0-based ascending index i of tridiag(alpha,0,alpha) (size n)
+ * by bisection on [lo, hi].  Stops when hi-lo <= max(2 eps max(|lo|,|hi|), atol)
+ * (atol = eps * g, LAPACK dstebz's absolute floor ulp*||T||; reading R9) or the
+ * midpoint stops moving.                                                      */
+double orc_bisect_one(int64_t n, const double* alpha, int64_t i, double lo, double hi, double pivmin, double atol) {
+  for (int it = 0; it < 2000; it++) {
+    double mid = 0.5 * (lo + hi);
+    if (hi - lo <= fmax(2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)), atol) || mid == lo || mid == hi) break;
+    if (orc_sturm_count(n, alpha, mid, pivmin) > i) hi = mid; else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+/* All eigenvalues with ascending indices [il, iu] of tridiag(alpha,0,alpha),
+ * written to lam[0 .. iu-il] ascending.                                      */
+void orc_bisect(int64_t n, const double* alpha, int64_t il, int64_t iu, double* lam) {
+  double g = orc_gershgorin(n, alpha);
+  double pivmin = orc_pivmin(n, alpha);
+  double bnd = g * (1.0 + 4.0 * DBL_EPSILON) + 4.0 * pivmin;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = il; i <= iu; i++) lam[i - il] = orc_bisect_one(n, alpha, i, -bnd, bnd, pivmin, DBL_EPSILON * g);
+}
+
+/* ------------------------------------------------------------------------- */
+/* O5: inverse iteration, dstein semantics ("inverse iteration").
+ * LU factorisation of (T - lambda I) with partial pivoting (LAPACK dlagtf) and
+ * the perturbed solve (LAPACK dlagts, job = -1).  T = tridiag(e, 0, e), size m.  */
+typedef struct { double *a, *b, *c, *d; int *in; } orc_lu;
+
+static void orc_lagtf(int64_t m, const double* e, double lambda, orc_lu* f) {
+  for (int64_t k = 0; k < m; k++) { f->a[k] = -lambda; f->in[k] = 0; }
+  for (int64_t k = 0; k + 1 < m; k++) { f->b[k] = e[k]; f->c[k] = e[k]; }
+  if (m == 1) return;
+  for (int64_t k = 0; k + 1 < m; k++) {
+    double scale1 = fabs(f->a[k]) + fabs(f->b[k]);
+    double scale2 = fabs(f->c[k]) + fabs(f->a[k + 1]) + (k + 2 < m ? fabs(f->b[k + 1]) : 0.0);
+    double piv1 = (scale1 == 0.0) ? 0.0 : fabs(f->a[k]) / scale1;
+    if (f->c[k] == 0.0) {
+      f->in[k] = 0;
+      if (k + 2 < m) f->d[k] = 0.0;
+    } else {
+      double piv2 = fabs(f->c[k]) / scale2;
+      if (piv2 <= piv1) {
+        f->in[k] = 0;
+        f->c[k] = f->c[k] / f->a[k];
+        f->a[k + 1] -= f->c[k] * f->b[k];
+        if (k + 2 < m) f->d[k] = 0.0;
+      } else {
+        f->in[k] = 1;
+        double mult = f->a[k] / f->c[k];
+        f->a[k] = f->c[k];
+        double temp = f->a[k + 1];
+        f->a[k + 1] = f->b[k] - mult * temp;
+        if (k + 2 < m) {
+          f->d[k] = f->b[k + 1];
+          f->b[k + 1] = -mult * f->d[k];
+        }
+        f->b[k] = temp;
+        f->c[k] = mult;
+      }
+    }
+  }
+}
+
+static void orc_lagts(int64_t m, const orc_lu* f, double tol, double* y) {
+  const double sfmin = DBL_MIN, bignum = 1.0 / DBL_MIN;
+  for (int64_t k = 1; k < m; k++) {
+    if (f->in[k - 1] == 0) {
+      y[k] -= f->c[k - 1] * y[k - 1];
+    } else {
+      double temp = y[k - 1];
+      y[k - 1] = y[k];
+      y[k] = temp - f->c[k - 1] * y[k];
+    }
+  }
+  for (int64_t k = m - 1; k >= 0; k--) {
+    double temp;
+    if (k + 2 < m) temp = y[k] - f->b[k] * y[k + 1] - f->d[k] * y[k + 2];
+    else if (k + 1 < m) temp = y[k] - f->b[k] * y[k + 1];
+    else temp = y[k];
+    double ak = f->a[k];
+    double pert = copysign(tol, ak);
+    for (;;) {
+      double absak = fabs(ak);
+      if (absak < 1.0) {
+        if (absak < sfmin) {
+          if (absak == 0.0 || fabs(temp) * sfmin > absak) { ak += pert; pert *= 2.0; continue; }
+          temp *= bignum; ak *= bignum;
+        } else if (fabs(temp) > absak * bignum) { ak += pert; pert *= 2.0; continue; }
+      }
+      break;
+    }
+    y[k] = temp / ak;
+  }
+}
+
+static uint64_t orc_splitmix64(uint64_t x) {   /* start vectors (R9) */
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* Inverse iteration for ONE unreduced block T_b = tridiag(e, 0, e) (size m) and
+ * its eigenvalues lam[0..k-1] given in DESCENDING order.  Writes unit vectors to
+ * Z (m x k, ldz).  dstein steps: perturb lambda if closer than 10 eps g to the
+ * previous one; factor; up to 5 iterations of scale-solve with MGS against earlier
+ * members of the same cluster (gap < clus_tol); accept when ||y||_inf >=
+ * sqrt(0.1/m), then 2 extra iterations.  O6: then CGS2 (two classical Gram-Schmidt
+ * passes) against the previous `window` vectors and all earlier cluster members.
+ * start key for vector k: splitmix64(seed * golden + kglob0 + k, row).
+ * Returns the number of vectors that did not converge.                       */
+int64_t orc_inverse_iteration_block(int64_t m, const double* e, int64_t k, const double* lam_in,
+                                    double* Z, int64_t ldz, uint64_t seed, int64_t kglob0, int64_t window) {
+  int64_t nfail = 0;
+  if (m == 1) { for (int64_t c = 0; c < k; c++) Z[IDX(0, c, ldz)] = 1.0; return 0; }
+  double g = 0.0;
+  for (int64_t i = 0; i < m; i++) {
+    double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0);
+    if (r > g) g = r;
+  }
+  const double eps = DBL_EPSILON;
+  const double pertol = 10.0 * eps * g;
+  const double clus_tol = 1e-6 * g;
+  const double dtpcrt = sqrt(0.1 / (double)m);
+  orc_lu f;
+  f.a = (double*)malloc(sizeof(double) * m); f.b = (double*)malloc(sizeof(double) * m);
+  f.c = (double*)malloc(sizeof(double) * m); f.d = (double*)malloc(sizeof(double) * m);
+  f.in = (int*)malloc(sizeof(int) * m);
+  double* lam = (double*)malloc(sizeof(double) * (k > 0 ? k : 1));
+  double* y = (double*)malloc(sizeof(double) * m);
+  double* h = (double*)malloc(sizeof(double) * (k > 0 ? k : 1));
+  int64_t clus_start = 0;
+  for (int64_t c = 0; c < k; c++) {
+    double xj = lam_in[c];
+    if (c > 0) {
+      if (lam[c - 1] - xj < pertol) xj = lam[c - 1] - pertol;
+      if (lam_in[c - 1] - lam_in[c] >= clus_tol) clus_start = c;
+    } else clus_start = 0;
+    lam[c] = xj;
+    for (int64_t i = 0; i < m; i++) {
+      uint64_t z = orc_splitmix64(seed * 0x9E3779B97F4A7C15ull + (uint64_t)(kglob0 + c) * 0x100000001B3ull + (uint64_t)i);
+      y[i] = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+    }
+    orc_lagtf(m, e, xj, &f);
+    double tol = 0.0;
+    for (int64_t i = 0; i < m; i++) {
+      tol = fmax(tol, fabs(f.a[i]));
+      if (i + 1 < m) tol = fmax(tol, fabs(f.b[i]));
+      if (i + 2 < m) tol = fmax(tol, fabs(f.d[i]));
+    }
+    tol *= eps;
+    if (tol == 0.0) tol = eps;
+    int its = 0, nrmchk = 0, ok = 0;
+    while (its < 5) {
+      its++;
+      double asum = 0.0;
+      for (int64_t i = 0; i < m; i++) asum += fabs(y[i]);
+      double scl = (double)m * g * fmax(eps, fabs(f.a[m - 1])) / asum;
+      for (int64_t i = 0; i < m; i++) y[i] *= scl;
+      orc_lagts(m, &f, tol, y);
+      /* MGS against earlier members of this cluster */
+      for (int64_t p = clus_start; p < c; p++) {
+        double dot = 0.0;
+        for (int64_t i = 0; i < m; i++) dot += Z[IDX(i, p, ldz)] * y[i];
+        for (int64_t i = 0; i < m; i++) y[i] -= dot * Z[IDX(i, p, ldz)];
+      }
+      double nrm = 0.0;
+      for (int64_t i = 0; i < m; i++) if (fabs(y[i]) > nrm) nrm = fabs(y[i]);
+      if (nrm < dtpcrt) continue;
+      nrmchk++;
+      if (nrmchk < 3) continue;
+      ok = 1;
+      break;
+    }
+    if (!ok) nfail++;
+    /* O6: CGS2 against previous `window` vectors and the earlier cluster members */
+    int64_t p0 = c - window;
+    if (p0 < 0) p0 = 0;
+    if (clus_start < p0) p0 = clus_start;
+    for (int pass = 0; pass < 2; pass++) {
+      double nrm2 = 0.0;
+      for (int64_t i = 0; i < m; i++) nrm2 += y[i] * y[i];
+      double s = 1.0 / sqrt(nrm2);
+      for (int64_t i = 0; i < m; i++) y[i] *= s;
+      for (int64_t p = p0; p < c; p++) {
+        double dot = 0.0;
+        for (int64_t i = 0; i < m; i++) dot += Z[IDX(i, p, ldz)] * y[i];
+        h[p] = dot;
+      }
+      for (int64_t p = p0; p < c; p++)
+        for (int64_t i = 0; i < m; i++) y[i] -= h[p] * Z[IDX(i, p, ldz)];
+    }
+    double nrm2 = 0.0;
+    for (int64_t i = 0; i < m; i++) nrm2 += y[i] * y[i];
+    double s = 1.0 / sqrt(nrm2);
+    /* sign: largest-magnitude entry positive (dstein) */
+    int64_t jmax = 0;
+    for (int64_t i = 1; i < m; i++) if (fabs(y[i]) > fabs(y[jmax])) jmax = i;
+    if (y[jmax] < 0) s = -s;
+    for (int64_t i = 0; i < m; i++) Z[IDX(i, c, ldz)] = y[i] * s;
+  }
+  free(f.a); free(f.b); free(f.c); free(f.d); free(f.in); free(lam); free(y); free(h);
+  return nfail;
+}
+
+/* Top-nev eigenpairs of T_sym = tridiag(alpha, 0, alpha) (size n): split into
+ * unreduced blocks where alpha_k == 0 exactly (O3), per block bisection for its
+ * top min(nev, m_b) eigenvalues, merge, keep the nev largest (descending; ties
+ * by block order), then inverse iteration per block (O5/O6).
+ * lam (nev) descending; Q (n x nev, ldq) the eigenvectors (zero outside the block).
+ * Returns the number of non-converged vectors (SKEW status NOCONV if > 0).    */
+int64_t orc_tridiag_eig(int64_t n, const double* alpha, int64_t nev, double* lam, double* Q, int64_t ldq,
+                        uint64_t seed, int64_t window, int want_vectors) {
+  if (nev <= 0) return 0;
+  int64_t nblk = 0;
+  int64_t* bs = (int64_t*)malloc(sizeof(int64_t) * (n + 1));
+  bs[0] = 0;
+  for (int64_t k = 0; k + 1 < n; k++) if (alpha[k] == 0.0) bs[++nblk] = k + 1;
+  bs[++nblk] = n;
+  /* candidates */
+  int64_t ncand = 0;
+  for (int64_t b = 0; b < nblk; b++) { int64_t mb = bs[b + 1] - bs[b]; ncand += (mb < nev ? mb : nev); }
+  double* cl = (double*)malloc(sizeof(double) * ncand);
+  int64_t* cb = (int64_t*)malloc(sizeof(int64_t) * ncand);
+  int64_t pos = 0;
+  for (int64_t b = 0; b < nblk; b++) {
+    int64_t s0 = bs[b], mb = bs[b + 1] - bs[b];
+    int64_t kb = mb < nev ? mb : nev;
+    double* tmp = (double*)malloc(sizeof(double) * kb);
+    if (mb == 1) tmp[0] = 0.0;
+    else orc_bisect(mb, alpha + s0, mb - kb, mb - 1, tmp);
+    for (int64_t i = 0; i < kb; i++) { cl[pos] = tmp[kb - 1 - i]; cb[pos] = b; pos++; }  /* descending */
+    free(tmp);
+  }
+  /* stable selection of the nev largest (insertion order = block order) */
+  int64_t* ord = (int64_t*)malloc(sizeof(int64_t) * ncand);
+  for (int64_t i = 0; i < ncand; i++) ord[i] = i;
+  for (int64_t i = 1; i < ncand; i++) {   /* stable insertion sort, descending value */
+    int64_t t = ord[i], j = i - 1;
+    while (j >= 0 && cl[ord[j]] < cl[t]) { ord[j + 1] = ord[j]; j--; }
+    ord[j + 1] = t;
+  }
+  for (int64_t i = 0; i < nev; i++) lam[i] = cl[ord[i]];
+  int64_t nfail = 0;
+  if (want_vectors) {
+    for (int64_t c = 0; c < nev; c++) for (int64_t i = 0; i < n; i++) Q[IDX(i, c, ldq)] = 0.0;
+    /* per block: gather its selected eigenvalues (already descending in output order) */
+    int64_t* sel = (int64_t*)malloc(sizeof(int64_t) * nev);
+    for (int64_t b = 0; b < nblk; b++) {
+      int64_t s0 = bs[b], mb = bs[b + 1] - bs[b], kk = 0;
+      for (int64_t i = 0; i < nev; i++) if (cb[ord[i]] == b) sel[kk++] = i;
+      if (kk == 0) continue;
+      double* lb = (double*)malloc(sizeof(double) * kk);
+      double* Zb = (double*)malloc(sizeof(double) * (size_t)mb * kk);
+      for (int64_t i = 0; i < kk; i++) lb[i] = lam[sel[i]];
+      nfail += orc_inverse_iteration_block(mb, alpha + s0, kk, lb, Zb, mb, seed, sel[0], window);
+      for (int64_t i = 0; i < kk; i++)
+        for (int64_t r = 0; r < mb; r++) Q[IDX(s0 + r, sel[i], ldq)] = Zb[IDX(r, i, mb)];
+      free(lb); free(Zb);
+    }
+    free(sel);
+  }
+  free(bs); free(cl); free(cb); free(ord);
+  return nfail;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O7: Q <- D Q_diag, D = diag(i^0, i^1, ..., i^{n-1})  (Lemma 1, reading R1;
+ * Alg. 1 step 3).  Row k of q goes to Re (sign +) for
+ * k%4 == 0, Im (+) for 1, Re (-) for 2, Im (-) for 3.                         */
+void orc_apply_D(int64_t n, int64_t nev, const double* Q, int64_t ldq, double* Xre, double* Xim, int64_t ldx) {
+  for (int64_t c = 0; c < nev; c++)
+    for (int64_t k = 0; k < n; k++) {
+      double q = Q[IDX(k, c, ldq)], re = 0.0, im = 0.0;
+      switch (k & 3) {
+        case 0: re = q; break;
+        case 1: im = q; break;
+        case 2: re = -q; break;
+        default: im = -q; break;
+      }
+      Xre[IDX(k, c, ldx)] = re;
+      Xim[IDX(k, c, ldx)] = im;
+    }
+}
+
+/* O8: X <- Q_trd X, Q_trd = H_0 H_1 ... H_{n-3}, H_j = I - tau_j v_j v_j^T with
+ * v_j stored in A[j+2:, j] (v_j[0] = 1 at row j+1).  Applied to real columns
+ * (Re and Im planes independently), H_{n-3} first.          */
+void orc_backtransform(int64_t n, const double* A, int64_t lda, const double* tau, int64_t ncols,
+                       double* X, int64_t ldx) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < ncols; c++) {
+    double* x = &X[IDX(0, c, ldx)];
+    for (int64_t j = n - 3; j >= 0; j--) {
+      double t = tau[j];
+      if (t == 0.0) continue;
+      const double* v = &A[IDX(j + 1, j, lda)];   /* v[0] is beta in storage; use 1 */
+      double s = x[j + 1];
+      for (int64_t i = 1; i < n - j - 1; i++) s += v[i] * x[j + 1 + i];
+      s *= t;
+      x[j + 1] -= s;
+      for (int64_t i = 1; i < n - j - 1; i++) x[j + 1 + i] -= s * v[i];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Full oracle solve (Algorithm 1 steps 1-4; half spectrum,
+ * PAPER.md:228-233).  A: strictly-lower input (lda), NOT modified (copied).
+ * lambda (nev) descending >= 0; Zre/Zim n x nev (ldz) with A z = i lambda z,
+ * ||z|| = 1.  want_vectors = 0: eigenvalues only (stops after O4).
+ * times (optional, 4 doubles): seconds for O2, O4, O5-O6, O7-O8.
+ * Returns: 0 ok, -k bad argument k, >0 number of non-converged vectors.      */
+#include <time.h>
+static double orc_now(void) { struct timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec + 1e-9 * t.tv_nsec; }
+
+int64_t orc_skew_eig(int64_t n, const double* A, int64_t lda, int64_t nev, double* lambda,
+                     double* Zre, double* Zim, int64_t ldz, int want_vectors, uint64_t seed, double* times) {
+  if (n < 1) return -1;
+  if (lda < n) return -3;
+  if (nev < 0 || nev > n / 2) return -4;
+  if (want_vectors && ldz < n) return -8;
+  double t0 = orc_now();
+  double* W = (double*)malloc(sizeof(double) * (size_t)n * n);
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) W[IDX(i, j, n)] = (i > j) ? A[IDX(i, j, lda)] : 0.0;
+  double* alpha = (double*)calloc((size_t)(n > 1 ? n - 1 : 1), sizeof(double));
+  double* tau = (double*)calloc((size_t)(n > 1 ? n - 1 : 1), sizeof(double));
+  orc_tridiagonalize(n, W, n, alpha, tau);
+  double t1 = orc_now();
+  double* Q = want_vectors ? (double*)malloc(sizeof(double) * (size_t)n * (nev > 0 ? nev : 1)) : NULL;
+  int64_t nfail = orc_tridiag_eig(n, alpha, nev, lambda, Q, n, seed, 32, want_vectors);
+  double t2 = orc_now();
+  double t3 = t2;
+  if (want_vectors && nev > 0) {
+    double* X = (double*)malloc(sizeof(double) * (size_t)n * 2 * nev);
+    orc_apply_D(n, nev, Q, n, X, X + (size_t)n * nev, n);
+    t3 = orc_now();
+    orc_backtransform(n, W, n, tau, 2 * nev, X, n);
+    for (int64_t c = 0; c < nev; c++)
+      for (int64_t i = 0; i < n; i++) {
+        Zre[IDX(i, c, ldz)] = X[IDX(i, c, n)];
+        Zim[IDX(i, c, ldz)] = X[IDX(i, nev + c, n)];
+      }
+    free(X);
+  }
+  double t4 = orc_now();
+  if (times) { times[0] = t1 - t0; times[1] = t2 - t1; times[2] = t3 - t2; times[3] = t4 - t3; }
+  free(W); free(alpha); free(tau); if (Q) free(Q);
+  return nfail;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O0 (BSE steps 2-3).  Unblocked Cholesky M = L L^T (dpotf2
+ * order) from the lower triangle of M (n x n, ldm); L overwrites the lower
+ * triangle.  Pivot <= n eps max_i M_ii -> returns the 1-based failing pivot
+ * index (NotDefinite, reading R18); 0 on success.           */
+int64_t orc_cholesky(int64_t n, double* M, int64_t ldm) {
+  double dmax = 0.0;
+  for (int64_t i = 0; i < n; i++) if (M[IDX(i, i, ldm)] > dmax) dmax = M[IDX(i, i, ldm)];
+  double tol = (double)n * DBL_EPSILON * dmax;
+  for (int64_t j = 0; j < n; j++) {
+    double ajj = M[IDX(j, j, ldm)];
+    for (int64_t k = 0; k < j; k++) ajj -= M[IDX(j, k, ldm)] * M[IDX(j, k, ldm)];
+    if (!(ajj > tol)) return j + 1;
+    ajj = sqrt(ajj);
+    M[IDX(j, j, ldm)] = ajj;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = j + 1; i < n; i++) {
+      double s = M[IDX(i, j, ldm)];
+      for (int64_t k = 0; k < j; k++) s -= M[IDX(i, k, ldm)] * M[IDX(j, k, ldm)];
+      M[IDX(i, j, ldm)] = s / ajj;
+    }
+  }
+  return 0;
+}
+
+/* W = L^T J L with J = [[0, I], [-I, 0]], by its plain
+ * definition: JL is L with block rows swapped and the new lower block negated;
+ * W_ij = sum_k L_ki (JL)_kj, written to the strictly lower triangle of W
+ * (n x n, ldw).  L: lower triangle of (n x n, ldl); n even.                  */
+void orc_form_W(int64_t n, const double* L, int64_t ldl, double* W, int64_t ldw) {
+  int64_t m = n / 2;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t j = 0; j < n; j++) {
+    for (int64_t i = j + 1; i < n; i++) {
+      double s = 0.0;
+      for (int64_t k = i; k < n; k++) {     /* L_ki = 0 for k < i */
+        double Lki = L[IDX(k, i, ldl)];
+        /* (JL)_kj: k < m -> L_{k+m, j};  k >= m -> -L_{k-m, j}; lower-triangular L */
+        double jl;
+        if (k < m) { int64_t r = k + m; jl = (r >= j) ? L[IDX(r, j, ldl)] : 0.0; }
+        else { int64_t r = k - m; jl = (r >= j) ? -L[IDX(r, j, ldl)] : 0.0; }
+        s += Lki * jl;
+      }
+      W[IDX(i, j, ldw)] = s;
+    }
+  }
+}
