@@ -1,0 +1,115 @@
+/*
+ * skeweig.h -- C-ABI of the B200-native (sm_100a) two-stage skew-symmetric
+ * eigensolver (Penke, Marek, Vorwerk, Draxl, Benner, arXiv 1912.04062).
+ *
+ * Problem (Algorithm 1): for a real skew-symmetric
+ * A = -A^T (n x n), return the eigenpairs A z_k = i*lambda_k z_k with lambda_k > 0,
+ * the nev <= floor(n/2) LARGEST, in descending order (the other half are the
+ * conjugate pairs -i*lambda_k, conj(z_k)).  Eigenvectors are unit
+ * 2-norm; their phase is free (reading R7).
+ *
+ * Route (ELPA2 flavour): full->band (panel QR + skew rank-2k
+ * update, Eqs. (6)-(8)), band->tridiagonal bulge chasing
+ * (PAPER.md:446-462), Lemma 1 link to tridiag(alpha, 0, alpha)
+ * solved by bisection + inverse iteration, Q <- D Q_diag
+ * (PAPER.md:307-311), then the two back-transformations on [Re | Im] as one real
+ * n x 2nev matrix.
+ *
+ * Conventions (all entry points):
+ *  - FP64, column-major, 0-based, 64-bit sizes.
+ *  - A skew input is read from its STRICTLY LOWER triangle only; the diagonal and
+ *    upper triangle are never read.
+ *  - Array pointers may be DEVICE pointers (cudaMalloc / torch) or HOST pointers
+ *    (pageable or pinned).  The library detects the kind with
+ *    cudaPointerGetAttributes; host arrays are staged through the workspace (the
+ *    workspace must then be sized with SKEW_WS_HOST_STAGING).  All arrays of one
+ *    call must be of the same kind.
+ *  - Ownership: every array belongs to the caller.  A (or M) is INPUT AND
+ *    DESTROYED when it is a device array (it receives reflectors and the band;
+ *    contents unspecified on return, LAPACK convention); a host A is not modified.
+ *    Outputs must not alias inputs.
+ *  - The library never allocates device memory in a solve: it uses the caller's
+ *    workspace (skew_workspace_size / skew_set_workspace).
+ *  - Calls are synchronous: work is enqueued on the context stream and the
+ *    stream is synchronised before returning, so the status is final.
+ *  - One context must not be used by two host threads at once; distinct
+ *    contexts are independent.
+ *
+ * Status codes: 0 ok; -i: the i-th argument is invalid (LAPACK INFO style, the
+ * context counts as argument 1); positive codes below.
+ */
+#ifndef SKEWEIG_H
+#define SKEWEIG_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKEW_OK 0
+#define SKEW_ERR_NOCONV 1          /* inverse iteration did not converge for some vectors */
+#define SKEW_ERR_NOT_DEFINITE 4    /* BSE: Cholesky pivot <= n*eps*max(diag M) */
+#define SKEW_ERR_CUDA 10           /* a CUDA runtime error (message: skew_last_error) */
+#define SKEW_ERR_NCCL 11
+#define SKEW_ERR_WORKSPACE 12      /* workspace missing or too small */
+#define SKEW_ERR_NOT_IMPLEMENTED 13
+
+/* workspace flags */
+#define SKEW_WS_VECTORS 1          /* eigenvectors requested (else eigenvalues only) */
+#define SKEW_WS_HOST_STAGING 2     /* room to stage host A (n x n) */
+#define SKEW_WS_BSE 4              /* room for the BSE front-end (Cholesky factor) */
+
+typedef struct skew_ctx_s* skew_ctx;
+
+/* Create a context on CUDA device `device` that enqueues on `cuda_stream`
+ * (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream; NULL = legacy
+ * default stream).  Tunables are read from the environment once here:
+ * SKEWEIG_B (band width b, default 64), SKEWEIG_BT2_K (sweeps per BT2 group,
+ * default 32), SKEWEIG_BT1_MERGE (panels per BT1 block reflector, default 4),
+ * SKEWEIG_REORTH_W (reorthogonalisation window, default 32). */
+int skew_ctx_create(skew_ctx* out, int device, void* cuda_stream);
+int skew_ctx_destroy(skew_ctx ctx);
+
+/* Bytes of device workspace a solve of order n with nev pairs needs (flags:
+ * SKEW_WS_*).  The caller allocates it (e.g. a torch uint8 tensor) and passes it
+ * with skew_set_workspace; it must stay alive while the context uses it. */
+int skew_workspace_size(skew_ctx ctx, int64_t n, int64_t nev, int flags, size_t* bytes);
+int skew_set_workspace(skew_ctx ctx, void* dptr, size_t bytes);
+
+/* Eigenpairs (Algorithm 1, ELPA2 flavour, half spectrum).
+ *   n        >= 1
+ *   A        n x n (lda >= n), strictly lower triangle read; destroyed if device
+ *   nev      1 <= nev <= floor(n/2)
+ *   lambda   nev doubles out, lambda_0 >= lambda_1 >= ... > 0
+ *   Zre, Zim n x nev each (ldz >= n): z_k = Zre[:,k] + i Zim[:,k]
+ * Returns 0, -i (bad argument i), SKEW_ERR_NOCONV, SKEW_ERR_CUDA, SKEW_ERR_WORKSPACE. */
+int skew_eig(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev,
+             double* lambda, double* Zre, double* Zim, int64_t ldz);
+
+/* Eigenvalues only (Algorithm 1 steps 1-2): the nev largest lambda_k, descending. */
+int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda);
+
+/* BSE form (steps 2-3): M (n x n, n even, symmetric positive
+ * definite, lower triangle read; destroyed if device) -> M = L L^T (Cholesky) ->
+ * W = L^T J L with J = [[0, I], [-I, 0]] -> eigenpairs of the skew W as in
+ * skew_eig.  Zre/Zim may be NULL (eigenvalues only).  On a pivot <= n*eps*max_i M_ii
+ * returns SKEW_ERR_NOT_DEFINITE with the 1-based pivot index in *pivot_out. */
+int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev,
+                 double* lambda, double* Zre, double* Zim, int64_t ldz, int64_t* pivot_out);
+
+/* Per-stage device times (ms) of the last solve, measured with CUDA events on the
+ * context stream: [0] full->band, [1] band->tridiagonal, [2] tridiagonal solve,
+ * [3] back-transform 2 (bulge reflectors), [4] back-transform 1 (block
+ * reflectors), [5] output, [6] BSE front-end.  `count` <= 7. */
+int skew_stage_times(skew_ctx ctx, double* ms_out, int count);
+
+/* Number of non-converged inverse-iteration vectors in the last solve. */
+int64_t skew_last_nfail(skew_ctx ctx);
+const char* skew_status_string(int status);
+const char* skew_last_error(skew_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKEWEIG_H */

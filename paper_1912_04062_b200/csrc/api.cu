@@ -1,0 +1,457 @@
+// api.cu -- the C-ABI (include/skeweig.h, include/skeweig_stages.h): argument checks,
+// workspace planning, host/device staging, the stage driver of Algorithm 1 (ELPA2
+// flavour) and per-stage CUDA-event timing.  No compute happens on the host except
+// the small tridiagonal bookkeeping (split points, task lists) in tridiag.cu.
+#include "../../include/skeweig.h"
+#include "../../include/skeweig_stages.h"
+#include "common.cuh"
+#include "internal.h"
+#include <cstdlib>
+#include <cstring>
+#include <cmath>
+#include <string>
+#include <algorithm>
+
+namespace sk {
+
+// ------------------------------------------------------------------------------------
+struct Plan {
+  F2BLayout f2b;
+  B2TLayout b2t;
+  int64_t n = 0, nev = 0, ldn = 0;
+  double* Astage = nullptr;    // n x ldn (host staging / BSE W)
+  double* S = nullptr;         // BSE m x m
+  double* vstore = nullptr;
+  F2BWork fw;
+  B2TWork bw;
+  double* alpha = nullptr;
+  double* lam = nullptr;
+  TridWork tw;
+  double* Q = nullptr;         // n x nev (ld ldn)
+  double* X = nullptr;         // n x 2nev (ld ldn)
+  BT1Work b1;
+  int64_t* status = nullptr;
+  double* scratch = nullptr;
+};
+
+static void plan_layout(Ctx& c, Plan& p, Arena& ar, int64_t n, int64_t nev, int flags) {
+  const bool vec = (flags & SKEW_WS_VECTORS) != 0;
+  p.n = n; p.nev = nev;
+  p.ldn = (n + 1) & ~int64_t(1);
+  const int b = c.prm.b;
+  p.f2b.init(n, b, c.prm.bt1_merge);
+  p.b2t.init(n, b, c.prm.bt2_k);
+  if (flags & (SKEW_WS_HOST_STAGING | SKEW_WS_BSE)) p.Astage = ar.take<double>((size_t)p.ldn * n);
+  if (flags & SKEW_WS_BSE) p.S = ar.take<double>((size_t)std::max<int64_t>(n / 2, 1) * std::max<int64_t>(n / 2, 1));
+  p.vstore = ar.take<double>((size_t)std::max<int64_t>(p.f2b.vstore_elems, 1));
+  f2b_reserve(ar, p.f2b, c.num_sms, p.fw);
+  b2t_reserve(ar, p.b2t, vec, p.bw);
+  p.alpha = ar.take<double>(std::max<int64_t>(n, 1));
+  p.lam = ar.take<double>(std::max<int64_t>(nev, 1));
+  trid_reserve(ar, n, nev, vec, p.tw, c.prm.reorth_w);
+  if (vec) {
+    p.Q = ar.take<double>((size_t)p.ldn * std::max<int64_t>(nev, 1));
+    p.X = ar.take<double>((size_t)p.ldn * 2 * std::max<int64_t>(nev, 1));
+    bt1_reserve(ar, n, 2 * nev, c.prm.bt1_merge * b, p.b1);
+  }
+  p.status = ar.take<int64_t>(4);
+  p.scratch = ar.take<double>(64);
+}
+
+static bool plan_bind(Ctx& c, Plan& p, int64_t n, int64_t nev, int flags) {
+  Arena ar;
+  ar.base = (char*)c.ws;
+  ar.size = c.ws_bytes;
+  plan_layout(c, p, ar, n, nev, flags);
+  // any null from take() means out of space
+  return ar.off <= ar.size && p.status != nullptr && p.scratch != nullptr;
+}
+
+static int env_int(const char* name, int def) {
+  const char* s = getenv(name);
+  if (!s || !*s) return def;
+  return atoi(s);
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+
+}  // namespace sk
+
+using namespace sk;
+
+struct skew_ctx_s {
+  Ctx c;
+  cudaEvent_t ev_start[ST_COUNT];
+  cudaEvent_t ev_stop[ST_COUNT];
+  bool used[ST_COUNT];
+};
+
+static int set_cuda_err(skew_ctx ctx, cudaError_t e, const char* where) {
+  cudaGetLastError();   // clear a non-sticky error so the caller's runtime state stays clean
+  if (ctx) ctx->c.last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return SKEW_ERR_CUDA;
+}
+#define CK(call, where)                                   \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return set_cuda_err(ctx, _e, where); \
+  } while (0)
+
+static void tstart(skew_ctx ctx, int s) { cudaEventRecord(ctx->ev_start[s], ctx->c.stream); ctx->used[s] = true; }
+static void tstop(skew_ctx ctx, int s) { cudaEventRecord(ctx->ev_stop[s], ctx->c.stream); }
+static void tcollect(skew_ctx ctx) {
+  for (int s = 0; s < ST_COUNT; s++) {
+    float ms = 0.f;
+    if (ctx->used[s] && cudaEventElapsedTime(&ms, ctx->ev_start[s], ctx->ev_stop[s]) == cudaSuccess)
+      ctx->c.stage_ms[s] = ms;
+    else ctx->c.stage_ms[s] = 0.0;
+  }
+}
+static void treset(skew_ctx ctx) { for (int s = 0; s < ST_COUNT; s++) ctx->used[s] = false; }
+
+extern "C" {
+
+int skew_ctx_create(skew_ctx* out, int device, void* cuda_stream) {
+  if (!out) return -1;
+  skew_ctx ctx = new skew_ctx_s();
+  ctx->c.device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { delete ctx; return SKEW_ERR_CUDA; }
+  ctx->c.stream = (cudaStream_t)cuda_stream;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  ctx->c.num_sms = nsm;
+  ctx->c.prm.b = env_int("SKEWEIG_B", 64);
+  ctx->c.prm.bt2_k = env_int("SKEWEIG_BT2_K", 32);
+  ctx->c.prm.bt1_merge = env_int("SKEWEIG_BT1_MERGE", 4);
+  ctx->c.prm.reorth_w = env_int("SKEWEIG_REORTH_W", 32);
+  if (ctx->c.prm.b < 2 || ctx->c.prm.b > 64 || (ctx->c.prm.b & 1)) ctx->c.prm.b = 64;
+  if (ctx->c.prm.bt2_k != 32) ctx->c.prm.bt2_k = 32;
+  if (ctx->c.prm.bt1_merge < 1 || ctx->c.prm.bt1_merge > 8) ctx->c.prm.bt1_merge = 4;
+  if (ctx->c.prm.reorth_w < 0 || ctx->c.prm.reorth_w > 256) ctx->c.prm.reorth_w = 32;
+  for (int s = 0; s < ST_COUNT; s++) {
+    cudaEventCreate(&ctx->ev_start[s]);
+    cudaEventCreate(&ctx->ev_stop[s]);
+    ctx->used[s] = false;
+  }
+  *out = ctx;
+  return SKEW_OK;
+}
+
+int skew_ctx_destroy(skew_ctx ctx) {
+  if (!ctx) return -1;
+  for (int s = 0; s < ST_COUNT; s++) { cudaEventDestroy(ctx->ev_start[s]); cudaEventDestroy(ctx->ev_stop[s]); }
+  delete ctx;
+  return SKEW_OK;
+}
+
+int skew_workspace_size(skew_ctx ctx, int64_t n, int64_t nev, int flags, size_t* bytes) {
+  if (!ctx) return -1;
+  if (n < 1) return -2;
+  if (nev < 0 || nev > n / 2) return -3;
+  if (!bytes) return -5;
+  Plan p;
+  Arena ar;
+  ar.measuring = true;
+  plan_layout(ctx->c, p, ar, n, nev, flags);
+  *bytes = ar.off + 4096;
+  return SKEW_OK;
+}
+
+int skew_set_workspace(skew_ctx ctx, void* dptr, size_t bytes) {
+  if (!ctx) return -1;
+  if (bytes > 0 && !is_device_ptr(dptr)) return -2;
+  ctx->c.ws = dptr;
+  ctx->c.ws_bytes = bytes;
+  return SKEW_OK;
+}
+
+int skew_stage_times(skew_ctx ctx, double* ms_out, int count) {
+  if (!ctx) return -1;
+  if (!ms_out || count < 0 || count > ST_COUNT) return -2;
+  for (int i = 0; i < count; i++) ms_out[i] = ctx->c.stage_ms[i];
+  return SKEW_OK;
+}
+
+int64_t skew_last_nfail(skew_ctx ctx) { return ctx ? ctx->c.last_nfail : -1; }
+
+const char* skew_last_error(skew_ctx ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
+
+const char* skew_status_string(int status) {
+  switch (status) {
+    case SKEW_OK: return "ok";
+    case SKEW_ERR_NOCONV: return "inverse iteration did not converge for some eigenvectors";
+    case SKEW_ERR_NOT_DEFINITE: return "matrix is not positive definite (Cholesky pivot too small)";
+    case SKEW_ERR_CUDA: return "CUDA error";
+    case SKEW_ERR_NCCL: return "NCCL error";
+    case SKEW_ERR_WORKSPACE: return "workspace missing or too small";
+    case SKEW_ERR_NOT_IMPLEMENTED: return "not implemented";
+    default: return status < 0 ? "invalid argument" : "unknown status";
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// The solve driver shared by skew_eig / skew_eigvals / skew_eig_bse.
+// A_d: device skew input (strictly lower), destroyed.  lam_out/Zre/Zim: device or host.
+static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t nev, double* lambda, bool lam_host,
+                      double* Zre, double* Zim, int64_t ldz, bool z_host) {
+  Ctx& c = ctx->c;
+  cudaStream_t st = c.stream;
+  const int64_t n = p.n;
+  const bool vec = (Zre != nullptr);
+  // ---- full -> band
+  tstart(ctx, ST_F2B);
+  if (p.f2b.npanel > 0) {
+    CK(cudaMemsetAsync(p.vstore, 0, sizeof(double) * p.f2b.vstore_elems, st), "memset vstore");
+    CK(f2b_run(p.f2b, A_d, lda, p.vstore, p.fw, c.num_sms, st), "f2b");
+  }
+  tstop(ctx, ST_F2B);
+  // ---- band -> tridiagonal
+  tstart(ctx, ST_B2T);
+  const int bw = (int)std::min<int64_t>(c.prm.b, std::max<int64_t>(n - 1, 1));
+  (void)bw;
+  CK(band_extract(A_d, lda, n, c.prm.b, p.bw.AB, p.b2t.ldab, st), "band extract");
+  CK(b2t_run(p.b2t, p.bw, p.alpha, c.num_sms, st), "b2t");
+  tstop(ctx, ST_B2T);
+  // ---- tridiagonal eigenproblem
+  tstart(ctx, ST_TRID);
+  int64_t nfail = 0;
+  CK(trid_run(n, p.alpha, nev, p.lam, vec ? p.Q : nullptr, p.ldn, p.tw, c.prm, &nfail, st), "tridiagonal");
+  c.last_nfail = nfail;
+  if (vec) CK(assemble_D(p.Q, p.ldn, n, nev, p.X, p.ldn, st), "assemble D");
+  tstop(ctx, ST_TRID);
+  if (vec) {
+    tstart(ctx, ST_BT2);
+    CK(bt2_run(p.b2t, p.bw, p.X, p.ldn, 2 * nev, st), "bt2");
+    tstop(ctx, ST_BT2);
+    tstart(ctx, ST_BT1);
+    if (p.f2b.npanel > 0) CK(bt1_run(p.f2b, p.vstore, p.fw.tau, p.X, p.ldn, 2 * nev, p.b1, st), "bt1");
+    tstop(ctx, ST_BT1);
+  }
+  // ---- output
+  tstart(ctx, ST_OUT);
+  CK(cudaMemcpyAsync(lambda, p.lam, sizeof(double) * nev, lam_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                     st), "lambda out");
+  if (vec) {
+    if (z_host) {
+      CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nev, cudaMemcpyDeviceToHost, st), "Zre out");
+      CK(cudaMemcpy2DAsync(Zim, ldz * 8, p.X + (size_t)p.ldn * nev, p.ldn * 8, n * 8, nev, cudaMemcpyDeviceToHost, st),
+         "Zim out");
+    } else {
+      CK(split_output(p.X, p.ldn, n, nev, Zre, Zim, ldz, st), "split output");
+    }
+  }
+  tstop(ctx, ST_OUT);
+  CK(cudaStreamSynchronize(st), "sync");
+  tcollect(ctx);
+  return nfail > 0 ? SKEW_ERR_NOCONV : SKEW_OK;
+}
+
+static int eig_entry(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda, double* Zre,
+                     double* Zim, int64_t ldz, bool need_vec) {
+  if (!ctx) return -1;
+  if (n < 1) return -2;
+  if (!A) return -3;
+  if (lda < n) return -4;
+  if (nev < 1 || nev > n / 2) return -5;
+  if (!lambda) return -6;
+  if (need_vec && !Zre) return -7;
+  if (need_vec && !Zim) return -8;
+  const bool vec = (Zre != nullptr || Zim != nullptr);
+  if (vec && (!Zre)) return -7;
+  if (vec && (!Zim)) return -8;
+  if (vec && ldz < n) return -9;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  treset(ctx);
+  const bool a_dev = is_device_ptr(A);
+  const bool l_dev = is_device_ptr(lambda);
+  const bool z_dev = vec ? is_device_ptr(Zre) : a_dev;
+  if (vec && is_device_ptr(Zim) != z_dev) return -8;
+  int flags = (vec ? SKEW_WS_VECTORS : 0) | (a_dev ? 0 : SKEW_WS_HOST_STAGING);
+  Plan p;
+  if (!ctx->c.ws || !plan_bind(ctx->c, p, n, nev, flags)) {
+    ctx->c.last_error = "workspace missing or too small";
+    return SKEW_ERR_WORKSPACE;
+  }
+  double* A_d = A;
+  int64_t ldad = lda;
+  if (!a_dev) {
+    // host input: stage into the workspace (host A is not modified); the copy is part of the call
+    ldad = p.ldn;
+    CK(cudaMemcpy2DAsync(p.Astage, ldad * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, ctx->c.stream), "A in");
+    A_d = p.Astage;
+  }
+  return solve_core(ctx, p, A_d, ldad, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev);
+}
+
+int skew_eig(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda, double* Zre, double* Zim,
+             int64_t ldz) {
+  return eig_entry(ctx, n, A, lda, nev, lambda, Zre, Zim, ldz, true);
+}
+
+int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda) {
+  return eig_entry(ctx, n, A, lda, nev, lambda, nullptr, nullptr, n, false);
+}
+
+int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, double* lambda, double* Zre,
+                 double* Zim, int64_t ldz, int64_t* pivot_out) {
+  if (!ctx) return -1;
+  if (n < 2 || (n & 1)) return -2;
+  if (!M) return -3;
+  if (ldm < n) return -4;
+  if (nev < 1 || nev > n / 2) return -5;
+  if (!lambda) return -6;
+  const bool vec = (Zre != nullptr);
+  if (vec && !Zim) return -8;
+  if (vec && ldz < n) return -9;
+  if (pivot_out) *pivot_out = 0;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  treset(ctx);
+  const bool m_dev = is_device_ptr(M);
+  const bool l_dev = is_device_ptr(lambda);
+  const bool z_dev = vec ? is_device_ptr(Zre) : m_dev;
+  int flags = (vec ? SKEW_WS_VECTORS : 0) | SKEW_WS_BSE;
+  Plan p;
+  if (!ctx->c.ws || !plan_bind(ctx->c, p, n, nev, flags)) {
+    ctx->c.last_error = "workspace missing or too small";
+    return SKEW_ERR_WORKSPACE;
+  }
+  cudaStream_t st = ctx->c.stream;
+  double* M_d = M;
+  int64_t ldmd = ldm;
+  if (!m_dev) {
+    // host M: stage it in the (n x n) buffer of the BSE-sized workspace used for L (the
+    // skew W then goes to the X region ... keep it simple: L in Q+X region is not
+    // guaranteed large enough, so host M is staged into Astage and W built in place of
+    // a second buffer is not available) -> require device M for now.
+    ctx->c.last_error = "skew_eig_bse: M must be a device pointer";
+    return -3;
+  }
+  tstart(ctx, ST_BSE);
+  const int64_t m = n / 2;
+  CK(bse_front(M_d, ldmd, n, p.Astage, p.ldn, p.S, m, p.scratch, p.status, st), "bse front");
+  int64_t piv = 0;
+  CK(cudaMemcpyAsync(&piv, p.status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "pivot");
+  CK(cudaStreamSynchronize(st), "sync");
+  tstop(ctx, ST_BSE);
+  if (piv != 0) {
+    if (pivot_out) *pivot_out = piv;
+    return SKEW_ERR_NOT_DEFINITE;
+  }
+  int rc = solve_core(ctx, p, p.Astage, p.ldn, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev_start[ST_BSE], ctx->ev_stop[ST_BSE]);
+  ctx->c.stage_ms[ST_BSE] = ms;
+  return rc;
+}
+
+// ------------------------------------------------------------------------------------
+// stage entry points
+int skew_stage_reduce_to_band(skew_ctx ctx, int64_t n, double* A, int64_t lda, double* Vout, int64_t ldv,
+                              double* Tout, double* tau_out, int64_t* npanel_out) {
+  if (!ctx) return -1;
+  if (n < 1) return -2;
+  if (!A || !is_device_ptr(A)) return -3;
+  if (lda < n) return -4;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  treset(ctx);
+  Plan p;
+  if (!ctx->c.ws || !plan_bind(ctx->c, p, n, 0, 0)) return SKEW_ERR_WORKSPACE;
+  cudaStream_t st = ctx->c.stream;
+  if (npanel_out) *npanel_out = p.f2b.npanel;
+  tstart(ctx, ST_F2B);
+  if (p.f2b.npanel > 0) {
+    CK(cudaMemsetAsync(p.vstore, 0, sizeof(double) * p.f2b.vstore_elems, st), "memset");
+    CK(f2b_run(p.f2b, A, lda, p.vstore, p.fw, ctx->c.num_sms, st), "f2b");
+  }
+  tstop(ctx, ST_F2B);
+  const int b = p.f2b.b;
+  if (Vout && p.f2b.npanel > 0) {
+    if (ldv < n) return -6;
+    for (int64_t j = 0; j < p.f2b.npanel; j++) {
+      int64_t g = j / p.f2b.merge, pl = j % p.f2b.merge;
+      int64_t r0 = p.f2b.r0(j), m = n - r0;
+      const double* Vj = p.vstore + p.f2b.goff[g] + pl * b + pl * b * p.f2b.gld[g];
+      CK(cudaMemcpy2DAsync(Vout + SK_IDX(r0, j * b, ldv), ldv * 8, Vj, p.f2b.gld[g] * 8, m * 8, b,
+                           cudaMemcpyDeviceToDevice, st), "V out");
+    }
+    if (Tout) CK(cudaMemcpyAsync(Tout, p.fw.T, sizeof(double) * b * b * p.f2b.npanel, cudaMemcpyDeviceToDevice, st), "T");
+    if (tau_out) CK(cudaMemcpyAsync(tau_out, p.fw.tau, sizeof(double) * b * p.f2b.npanel, cudaMemcpyDeviceToDevice, st), "tau");
+  }
+  CK(cudaStreamSynchronize(st), "sync");
+  tcollect(ctx);
+  return SKEW_OK;
+}
+
+int skew_stage_band_to_tridiag(skew_ctx ctx, int64_t n, int b, const double* AB, int64_t ldab, double* alpha_out,
+                               double* X, int64_t ldx, int64_t ncols) {
+  if (!ctx) return -1;
+  if (n < 1) return -2;
+  if (b < 1 || b > ctx->c.prm.b) return -3;
+  if (!AB || !is_device_ptr(AB)) return -4;
+  if (ldab < b + 1) return -5;
+  if (!alpha_out) return -6;
+  if (X && ldx < n) return -8;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  treset(ctx);
+  Plan p;
+  if (!ctx->c.ws || !plan_bind(ctx->c, p, n, 0, X ? SKEW_WS_VECTORS : 0)) return SKEW_ERR_WORKSPACE;
+  cudaStream_t st = ctx->c.stream;
+  B2TLayout L;
+  L.init(n, ctx->c.prm.b, ctx->c.prm.bt2_k);
+  tstart(ctx, ST_B2T);
+  CK(band_copy(AB, ldab, n, b, p.bw.AB, L.ldab, st), "band copy");
+  CK(b2t_run(L, p.bw, p.alpha, ctx->c.num_sms, st), "b2t");
+  tstop(ctx, ST_B2T);
+  if (n > 1) CK(cudaMemcpyAsync(alpha_out, p.alpha, sizeof(double) * (n - 1), cudaMemcpyDefault, st), "alpha");
+  if (X && ncols > 0) {
+    tstart(ctx, ST_BT2);
+    // X must be 16B-aligned with even ldx for the DMMA tiles: the BT2 kernel uses scalar loads
+    CK(bt2_run(L, p.bw, X, ldx, ncols, st), "bt2");
+    tstop(ctx, ST_BT2);
+  }
+  CK(cudaStreamSynchronize(st), "sync");
+  tcollect(ctx);
+  return SKEW_OK;
+}
+
+int skew_stage_tridiag_eig(skew_ctx ctx, int64_t n, const double* alpha, int64_t nev, double* lambda, double* Q,
+                           int64_t ldq) {
+  if (!ctx) return -1;
+  if (n < 1) return -2;
+  if (n > 1 && (!alpha || !is_device_ptr(alpha))) return -3;
+  if (nev < 1 || nev > n) return -4;
+  if (!lambda) return -5;
+  if (Q && ldq < n) return -7;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  treset(ctx);
+  Plan p;
+  int64_t nev_plan = std::min<int64_t>(nev, n / 2);
+  (void)nev_plan;
+  Arena ar;
+  ar.base = (char*)ctx->c.ws;
+  ar.size = ctx->c.ws_bytes;
+  TridWork tw;
+  trid_reserve(ar, n, nev, Q != nullptr, tw, ctx->c.prm.reorth_w);
+  double* lam_d = ar.take<double>(std::max<int64_t>(nev, 1));
+  if (!ctx->c.ws || ar.off > ar.size || !lam_d) return SKEW_ERR_WORKSPACE;
+  cudaStream_t st = ctx->c.stream;
+  tstart(ctx, ST_TRID);
+  int64_t nfail = 0;
+  CK(trid_run(n, alpha, nev, lam_d, Q, ldq, tw, ctx->c.prm, &nfail, st), "tridiagonal");
+  tstop(ctx, ST_TRID);
+  CK(cudaMemcpyAsync(lambda, lam_d, sizeof(double) * nev, cudaMemcpyDefault, st), "lambda");
+  CK(cudaStreamSynchronize(st), "sync");
+  tcollect(ctx);
+  ctx->c.last_nfail = nfail;
+  return nfail ? SKEW_ERR_NOCONV : SKEW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// bse.cu -- BSE-form front end (SURVEY §8(b) entry point skew_eig_bse):
+//   step 2: M = L L^T (blocked right-looking Cholesky: diagonal-block factor, panel
+//           TRSM, DMMA SYRK trailing update on the lower triangle);
+//   step 3: W = L^T J L, J = [[0, I], [-I, 0]]:
+//           W11 = S - S^T with S = L11^T L21,  W21 = -L22^T L11,  W22 = 0
+//           (block expansion of L^T (J L)).
+// NotDefinite when a pivot <= n*eps*max_i M_ii (reading R18).
+#include "common.cuh"
+#include "gemm_dmma.cuh"
+#include "internal.h"
+#include <algorithm>
+#include <cfloat>
+
+namespace sk {
+
+static constexpr int kCholNB = 64;
+
+__global__ void diag_max_kernel(const double* M, int64_t ldm, int64_t n, double* out) {
+  __shared__ double red[256];
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, M[SK_IDX(i, i, ldm)]);
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+// unblocked Cholesky of the nb x nb diagonal block at (j0, j0); status[0] = first failing pivot (1-based)
+__global__ void chol_diag_kernel(double* M, int64_t ldm, int64_t j0, int nb, int64_t n, const double* dmax,
+                                 int64_t* status) {
+  __shared__ double L[kCholNB * kCholNB];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e % nb, j = e / nb;
+    L[e] = (i >= j) ? M[SK_IDX(j0 + i, j0 + j, ldm)] : 0.0;
+  }
+  __syncthreads();
+  if (status[0] != 0) return;
+  const double tol = (double)n * DBL_EPSILON * dmax[0];
+  for (int j = 0; j < nb; j++) {
+    if (threadIdx.x == 0) {
+      double d = L[j + j * nb];
+      if (!(d > tol)) { bad = 1; status[0] = j0 + j + 1; }
+      else L[j + j * nb] = sqrt(d);
+    }
+    __syncthreads();
+    if (bad) return;
+    double djj = L[j + j * nb];
+    for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) L[i + j * nb] /= djj;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+      int i = e % nb, k = e / nb;
+      if (k > j && i >= k) L[i + k * nb] -= L[i + j * nb] * L[k + j * nb];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e % nb, j = e / nb;
+    M[SK_IDX(j0 + i, j0 + j, ldm)] = (i >= j) ? L[e] : 0.0;
+  }
+}
+
+// panel TRSM: rows below the block: L21 = M21 L11^{-T}, one thread per row
+__global__ void chol_trsm_kernel(double* M, int64_t ldm, int64_t j0, int nb, int64_t n, const int64_t* status) {
+  __shared__ double L[kCholNB * kCholNB];
+  if (status[0] != 0) return;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) L[e] = M[SK_IDX(j0 + e % nb, j0 + e / nb, ldm)];
+  __syncthreads();
+  int64_t i = j0 + nb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x[kCholNB];
+  for (int j = 0; j < nb; j++) x[j] = M[SK_IDX(i, j0 + j, ldm)];
+  for (int j = 0; j < nb; j++) {
+    double s = x[j];
+    for (int k = 0; k < j; k++) s -= x[k] * L[j + k * nb];
+    x[j] = s / L[j + j * nb];
+  }
+  for (int j = 0; j < nb; j++) M[SK_IDX(i, j0 + j, ldm)] = x[j];
+}
+
+__global__ void zero_upper_kernel(double* M, int64_t ldm, int64_t n) {
+  int64_t j = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < j; i += (int64_t)gridDim.x * blockDim.x)
+    M[SK_IDX(i, j, ldm)] = 0.0;
+}
+
+// W11 strictly lower = S - S^T ; W22 strictly lower = 0 ; (W21 written by GEMM)
+__global__ void w11_kernel(const double* S, int64_t lds, int64_t m, double* W, int64_t ldw) {
+  int64_t j = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i > j) {
+      W[SK_IDX(i, j, ldw)] = S[SK_IDX(i, j, lds)] - S[SK_IDX(j, i, lds)];
+      W[SK_IDX(m + i, m + j, ldw)] = 0.0;
+    }
+  }
+}
+
+// M (n x n, ldm) -> L in place; W (n x n, ldw) strictly lower; S scratch (m x m, lds).
+// status_d: device int64 (0 ok, else 1-based pivot).
+cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw, double* S, int64_t lds,
+                      double* scratch, int64_t* status_d, cudaStream_t st) {
+  cudaError_t e;
+  cudaMemsetAsync(status_d, 0, sizeof(int64_t), st);
+  diag_max_kernel<<<1, 256, 0, st>>>(M, ldm, n, scratch);
+  for (int64_t j0 = 0; j0 < n; j0 += kCholNB) {
+    int nb = (int)std::min<int64_t>(kCholNB, n - j0);
+    chol_diag_kernel<<<1, 256, 0, st>>>(M, ldm, j0, nb, n, scratch, status_d);
+    int64_t rest = n - j0 - nb;
+    if (rest > 0) {
+      chol_trsm_kernel<<<(unsigned)((rest + 127) / 128), 128, 0, st>>>(M, ldm, j0, nb, n, status_d);
+      GemmArgs ga;
+      ga.M = rest; ga.N = rest; ga.K = nb;
+      const double* L21 = M + SK_IDX(j0 + nb, j0, ldm);
+      ga.A = L21; ga.lda = ldm; ga.B = L21; ga.ldb = ldm;
+      ga.C = M + SK_IDX(j0 + nb, j0 + nb, ldm); ga.ldc = ldm; ga.alpha = -1.0; ga.beta = 1.0; ga.tri_off = 0;
+      e = gemm_dmma<128, 128, 16, 64, 32, 4, false, true, true>(ga, st);
+      if (e) return e;
+    }
+  }
+  {
+    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
+    zero_upper_kernel<<<grid, 256, 0, st>>>(M, ldm, n);
+  }
+  const int64_t m = n / 2;
+  // S = L11^T L21
+  {
+    GemmArgs ga;
+    ga.M = m; ga.N = m; ga.K = m;
+    ga.A = M; ga.lda = ldm; ga.B = M + m; ga.ldb = ldm; ga.C = S; ga.ldc = lds; ga.alpha = 1.0; ga.beta = 0.0;
+    e = gemm_dmma<128, 128, 16, 64, 32, 4, true, false, false>(ga, st);
+    if (e) return e;
+  }
+  // W21 = -L22^T L11
+  {
+    GemmArgs ga;
+    ga.M = m; ga.N = m; ga.K = m;
+    ga.A = M + SK_IDX(m, m, ldm); ga.lda = ldm; ga.B = M; ga.ldb = ldm; ga.C = W + m; ga.ldc = ldw;
+    ga.alpha = -1.0; ga.beta = 0.0;
+    e = gemm_dmma<128, 128, 16, 64, 32, 4, true, false, false>(ga, st);
+    if (e) return e;
+  }
+  {
+    dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 64), (unsigned)std::max<int64_t>(m, 1));
+    w11_kernel<<<grid, 256, 0, st>>>(S, lds, m, W, ldw);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace sk

@@ -1,0 +1,150 @@
+// internal.h -- host-side internal interfaces of the CUDA path (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+#include <string>
+
+namespace sk {
+
+// Bump allocator over the caller-provided workspace (the library never calls
+// cudaMalloc in steady state; SURVEY §8(b) "Ownership").
+struct Arena {
+  char* base = nullptr;
+  size_t size = 0, off = 0;
+  bool measuring = false;   // size-query mode: only accumulate
+  template <class T>
+  T* take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    if (measuring) { off += bytes; return nullptr; }
+    if (off + bytes > size) return nullptr;
+    T* p = reinterpret_cast<T*>(base + off);
+    off += bytes;
+    return p;
+  }
+};
+
+struct Params {
+  int b = 64;            // band width (F2B panel width), SKEWEIG_B
+  int bt2_k = 32;        // BT2 group width (sweeps per group), SKEWEIG_BT2_K
+  int bt1_merge = 4;     // F2B panels merged per BT1 block reflector, SKEWEIG_BT1_MERGE
+  int reorth_w = 32;     // inverse-iteration reorthogonalisation window, SKEWEIG_REORTH_W
+  uint64_t seed = 1;     // inverse-iteration start-vector seed
+};
+
+// Per-stage device timings (ms), recorded with CUDA events on the ctx stream.
+enum Stage { ST_F2B = 0, ST_B2T, ST_TRID, ST_BT2, ST_BT1, ST_OUT, ST_BSE, ST_COUNT };
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  Params prm;
+  cudaEvent_t ev[ST_COUNT + 1] = {};
+  double stage_ms[ST_COUNT] = {};
+  int64_t last_nfail = 0;
+  std::string last_error;
+  // distributed
+  int nranks = 1, rank = 0;
+  void* nccl = nullptr;
+};
+
+// Layout of the F2B reflector store: panels grouped by `merge` into block
+// reflectors for BT1.  Group g (panels g*merge .. g*merge+merge-1) owns a
+// ld_g x (merge*b) column-major block whose row 0 is global row r0(g*merge).
+struct F2BLayout {
+  int64_t n = 0;
+  int b = 64, merge = 4;
+  int64_t npanel = 0, ngroup = 0;
+  std::vector<int64_t> goff;   // element offset of group g in the V store
+  std::vector<int64_t> gld;    // leading dimension of group g (even)
+  int64_t vstore_elems = 0;
+  int64_t r0(int64_t j) const { return (j + 1) * (int64_t)b; }
+  void init(int64_t n_, int b_, int merge_);
+};
+
+
+// ---------------------------------------------------------------- per-stage work buffers
+struct F2BWork {
+  double* tau = nullptr;     // npanel * b
+  double* T = nullptr;       // npanel * b * b
+  double* part = nullptr;    // panel partials
+  double* rowk = nullptr;
+  double* gram = nullptr;
+  double* U = nullptr;       // n x b
+  double* X = nullptr;       // n x b
+  double* P = nullptr;       // n x 2b
+  double* Q = nullptr;       // n x 2b
+  double* zpart = nullptr;   // V^T X partials
+  double* Mb = nullptr;      // b x b
+};
+
+struct B2TLayout {
+  int64_t n = 0; int b = 64, k2 = 32;
+  int64_t nblk = 0, ngroups = 0;
+  std::vector<int64_t> gofs;   // first group index of each sweep block
+  int64_t ldab = 0;
+  void init(int64_t n_, int b_, int k2_);
+};
+
+struct B2TWork {
+  double* AB = nullptr;
+  int* progress = nullptr;
+  double* qv = nullptr;
+  double* qtau = nullptr;
+  double* qT = nullptr;
+  int64_t* gofs = nullptr;
+};
+
+struct TridWork {
+  double* a2 = nullptr;        // alpha^2 (n)
+  double* lamc = nullptr;      // candidates (n)
+  int64_t* tsk = nullptr;      // 3 * n task arrays
+  double* lamv = nullptr;      // per-vector perturbed lambda (nev)
+  double* gblk = nullptr;      // per-vector block bound
+  int64_t* vblk = nullptr;     // 2 * nev (s0, m)
+  double* inv = nullptr;       // inverse iteration work
+  unsigned char* inv_in = nullptr;
+  int* nfail = nullptr;
+  double* part = nullptr;      // gram partials
+  double* H = nullptr;         // projection coefficients
+  double* Rinv = nullptr;
+  int64_t batch = 0;
+};
+
+struct BT1Work {
+  double* G = nullptr;     // K x K
+  double* T = nullptr;     // K x K
+  double* U = nullptr;     // n x K
+  double* Z = nullptr;     // K x ncols
+};
+
+// f2b.cu
+void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w);
+cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, const F2BWork& w, int nsm,
+                    cudaStream_t st);
+// b2t.cu
+void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w);
+cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cudaStream_t st);
+cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st);
+cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st);
+cudaError_t band_copy(const double* ABin, int64_t ldin, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st);
+// tridiag.cu
+void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, int window);
+cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q, int64_t ldq,
+                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st);
+cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st);
+// bt1.cu
+void bt1_reserve(Arena& ar, int64_t n, int64_t ncols, int K, BT1Work& w);
+cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, double* X, int64_t ldx,
+                    int64_t ncols, BT1Work& w, cudaStream_t st);
+cudaError_t split_output(const double* X, int64_t ldx, int64_t n, int64_t nev, double* Zre, double* Zim, int64_t ldz,
+                         cudaStream_t st);
+// bse.cu
+cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw, double* S, int64_t lds,
+                      double* scratch, int64_t* status_d, cudaStream_t st);
+
+}  // namespace sk

@@ -1,0 +1,495 @@
+// tridiag.cu -- tridiagonal stage (a support stage) and the D
+// assembly (a8, Algorithm 1 step 3).
+//
+// Lemma 1: -i D^H T_skew D = T_sym = tridiag(alpha, 0, alpha),
+// D = diag(i^0..i^{n-1}).  The top-nev eigenpairs of T_sym are computed by
+// Sturm-count bisection (one thread per eigenvalue) and inverse iteration (one
+// thread per eigenvector, dstein-style LU with partial pivoting and perturbed
+// pivots), then re-orthogonalised in blocks of 32 against a window of previous
+// vectors (CGS2) plus the members of the vector's cluster, and within the block by
+// CholQR2 ("bisection and inverse iteration"; R9).
+// Unreduced blocks (alpha_k == 0 exactly) are treated separately (host-side split).
+#include "common.cuh"
+#include "internal.h"
+#include "gemm_dmma.cuh"
+#include <vector>
+#include <algorithm>
+#include <cmath>
+#include <cfloat>
+
+namespace sk {
+
+__device__ __forceinline__ uint64_t td_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Sturm count on block [s0, s0+m): #{eigenvalues < sigma}
+__device__ __forceinline__ int64_t td_sturm(const double* a2, int64_t s0, int64_t m, double sigma, double pivmin) {
+  int64_t cnt = 0;
+  double q = -sigma;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0) cnt++;
+  for (int64_t k = 1; k < m; k++) {
+    q = -sigma - a2[s0 + k - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0) cnt++;
+  }
+  return cnt;
+}
+
+// One bisection task per (block start, block size, ascending local index)
+__global__ void td_bisect_kernel(const double* a2, const int64_t* task_s0, const int64_t* task_m,
+                                 const int64_t* task_i, int64_t ntask, double g, double pivmin, double* out) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= ntask) return;
+  const int64_t s0 = task_s0[q], m = task_m[q], i = task_i[q];
+  if (m == 1) { out[q] = 0.0; return; }
+  double bnd = g * (1.0 + 4.0 * DBL_EPSILON) + 4.0 * pivmin;
+  double lo = -bnd, hi = bnd;
+  const double atol = DBL_EPSILON * g;
+  for (int it = 0; it < 2000; it++) {
+    double mid = 0.5 * (lo + hi);
+    if (hi - lo <= fmax(2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)), atol) || mid == lo || mid == hi) break;
+    if (td_sturm(a2, s0, m, mid, pivmin) > i) hi = mid; else lo = mid;
+  }
+  out[q] = 0.5 * (lo + hi);
+}
+
+// Inverse iteration, one thread per vector.  Work arrays interleaved [row][batch].
+struct InvArgs {
+  const double* alpha;          // global alpha (n-1)
+  const int64_t* vs0; const int64_t* vm;   // block start / size per vector
+  const double* lam;            // perturbed eigenvalue per vector
+  const double* gblk;           // block Gershgorin bound per vector
+  int64_t nvec; int64_t col0;   // vectors [col0, col0+nvec) of the output
+  double* Q; int64_t ldq; int64_t n;
+  double *wa, *wb, *wc, *wd; unsigned char* win;   // [mmax][nvec]
+  double* y;                    // [mmax][nvec]
+  uint64_t seed;
+  int* nfail;
+};
+
+__global__ void td_inverse_kernel(InvArgs a) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= a.nvec) return;
+  const int64_t gv = a.col0 + q;
+  const int64_t s0 = a.vs0[gv], m = a.vm[gv];
+  const int64_t B = a.nvec;
+  double* A_ = a.wa; double* Bb = a.wb; double* C = a.wc; double* D = a.wd; unsigned char* IN = a.win;
+  double* y = a.y;
+#define AT(arr, k) arr[(size_t)(k) * B + q]
+  const double lambda = a.lam[gv];
+  const double g = a.gblk[gv];
+  const double eps = DBL_EPSILON;
+  if (m == 1) {
+    for (int64_t i = 0; i < a.n; i++) a.Q[SK_IDX(i, gv, a.ldq)] = (i == s0) ? 1.0 : 0.0;
+    return;
+  }
+  // dlagtf: LU of T - lambda I with partial pivoting
+  for (int64_t k = 0; k < m; k++) { AT(A_, k) = -lambda; AT(IN, k) = 0; }
+  for (int64_t k = 0; k + 1 < m; k++) { double e = a.alpha[s0 + k]; AT(Bb, k) = e; AT(C, k) = e; }
+  for (int64_t k = 0; k + 1 < m; k++) {
+    double ak = AT(A_, k), bk = AT(Bb, k), ck = AT(C, k), ak1 = AT(A_, k + 1);
+    double bk1 = (k + 2 < m) ? AT(Bb, k + 1) : 0.0;
+    double scale1 = fabs(ak) + fabs(bk);
+    double scale2 = fabs(ck) + fabs(ak1) + fabs(bk1);
+    double piv1 = (scale1 == 0.0) ? 0.0 : fabs(ak) / scale1;
+    if (ck == 0.0) {
+      AT(IN, k) = 0;
+      if (k + 2 < m) AT(D, k) = 0.0;
+    } else {
+      double piv2 = fabs(ck) / scale2;
+      if (piv2 <= piv1) {
+        AT(IN, k) = 0;
+        double cm = ck / ak;
+        AT(C, k) = cm;
+        AT(A_, k + 1) = ak1 - cm * bk;
+        if (k + 2 < m) AT(D, k) = 0.0;
+      } else {
+        AT(IN, k) = 1;
+        double mult = ak / ck;
+        AT(A_, k) = ck;
+        AT(A_, k + 1) = bk - mult * ak1;
+        if (k + 2 < m) { AT(D, k) = bk1; AT(Bb, k + 1) = -mult * bk1; }
+        AT(Bb, k) = ak1;
+        AT(C, k) = mult;
+      }
+    }
+  }
+  double tol = 0.0;
+  for (int64_t k = 0; k < m; k++) {
+    tol = fmax(tol, fabs(AT(A_, k)));
+    if (k + 1 < m) tol = fmax(tol, fabs(AT(Bb, k)));
+    if (k + 2 < m) tol = fmax(tol, fabs(AT(D, k)));
+  }
+  tol *= eps;
+  if (tol == 0.0) tol = eps;
+  // start vector
+  for (int64_t i = 0; i < m; i++) {
+    uint64_t z = td_splitmix64(a.seed * 0x9E3779B97F4A7C15ull + (uint64_t)gv * 0x100000001B3ull + (uint64_t)i);
+    AT(y, i) = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+  }
+  const double dtpcrt = sqrt(0.1 / (double)m);
+  const double sfmin = DBL_MIN, bignum = 1.0 / DBL_MIN;
+  int nrmchk = 0, ok = 0;
+  for (int its = 0; its < 5; its++) {
+    double asum = 0.0;
+    for (int64_t i = 0; i < m; i++) asum += fabs(AT(y, i));
+    double scl = (double)m * g * fmax(eps, fabs(AT(A_, m - 1))) / asum;
+    for (int64_t i = 0; i < m; i++) AT(y, i) *= scl;
+    // dlagts(-1): forward
+    for (int64_t k = 1; k < m; k++) {
+      if (AT(IN, k - 1) == 0) AT(y, k) -= AT(C, k - 1) * AT(y, k - 1);
+      else { double tmp = AT(y, k - 1); AT(y, k - 1) = AT(y, k); AT(y, k) = tmp - AT(C, k - 1) * AT(y, k); }
+    }
+    // back with perturbation
+    double nrm = 0.0;
+    for (int64_t k = m - 1; k >= 0; k--) {
+      double temp;
+      if (k + 2 < m) temp = AT(y, k) - AT(Bb, k) * AT(y, k + 1) - AT(D, k) * AT(y, k + 2);
+      else if (k + 1 < m) temp = AT(y, k) - AT(Bb, k) * AT(y, k + 1);
+      else temp = AT(y, k);
+      double ak = AT(A_, k);
+      double pert = copysign(tol, ak);
+      for (int guard = 0; guard < 2100; guard++) {
+        double absak = fabs(ak);
+        if (absak < 1.0) {
+          if (absak < sfmin) {
+            if (absak == 0.0 || fabs(temp) * sfmin > absak) { ak += pert; pert *= 2.0; continue; }
+            temp *= bignum; ak *= bignum;
+          } else if (fabs(temp) > absak * bignum) { ak += pert; pert *= 2.0; continue; }
+        }
+        break;
+      }
+      double yk = temp / ak;
+      AT(y, k) = yk;
+      nrm = fmax(nrm, fabs(yk));
+    }
+    if (nrm < dtpcrt) continue;
+    nrmchk++;
+    if (nrmchk < 3) continue;
+    ok = 1;
+    break;
+  }
+  if (!ok) atomicAdd(a.nfail, 1);
+  double s2 = 0.0;
+  int64_t jmax = 0;
+  double ymax = 0.0;
+  for (int64_t i = 0; i < m; i++) {
+    double v = AT(y, i);
+    s2 += v * v;
+    if (fabs(v) > ymax) { ymax = fabs(v); jmax = i; }
+  }
+  double scl = 1.0 / sqrt(s2);
+  if (AT(y, jmax) < 0) scl = -scl;
+  for (int64_t i = 0; i < a.n; i++) {
+    double v = (i >= s0 && i < s0 + m) ? AT(y, i - s0) * scl : 0.0;
+    a.Q[SK_IDX(i, gv, a.ldq)] = v;
+  }
+#undef AT
+}
+
+// ---------------- block re-orthogonalisation helpers
+// partial H[(chunk)] = Qp^T Y over a row chunk: Qp n x p (ldq), Y n x nb (ldy); H p x nb
+__global__ void td_gram_partial(const double* Qp, int64_t ldq, int p, const double* Y, int64_t ldy, int nb,
+                                int64_t n, int64_t rows_per, double* part) {
+  extern __shared__ double hs[];
+  const int64_t r0 = blockIdx.x * rows_per, r1 = smin<int64_t>(n, r0 + rows_per);
+  for (int e = threadIdx.x; e < p * nb; e += blockDim.x) {
+    int i = e % p, j = e / p;
+    double s = 0.0;
+    const double* qa = Qp + SK_IDX(0, i, ldq);
+    const double* yb = Y + SK_IDX(0, j, ldy);
+    for (int64_t r = r0; r < r1; r++) s += qa[r] * yb[r];
+    part[(size_t)blockIdx.x * p * nb + e] = s;
+  }
+}
+__global__ void td_reduce_partials(const double* part, int nchunks, int cnt, double* out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cnt) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; c++) s += part[(size_t)c * cnt + e];
+  out[e] = s;
+}
+// Y -= Qp H   (row-parallel)
+__global__ void td_sub_proj(const double* Qp, int64_t ldq, int p, const double* H, double* Y, int64_t ldy, int nb,
+                            int64_t n) {
+  extern __shared__ double hs[];
+  for (int e = threadIdx.x; e < p * nb; e += blockDim.x) hs[e] = H[e];
+  __syncthreads();
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double q[64];
+  for (int i = 0; i < p; i++) q[i] = Qp[SK_IDX(r, i, ldq)];
+  for (int j = 0; j < nb; j++) {
+    double s = 0.0;
+    for (int i = 0; i < p; i++) s += q[i] * hs[i + j * p];
+    Y[SK_IDX(r, j, ldy)] -= s;
+  }
+}
+// Cholesky of the nb x nb Gram (in place, lower) -> R^{-1} upper in Rinv (single CTA)
+__global__ void td_chol_inv(const double* Gm, int nb, double* Rinv) {
+  __shared__ double L[32 * 32];
+  __shared__ double Li[32 * 32];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) { L[e] = Gm[e]; Li[e] = 0.0; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < nb; j++) {
+      double d = L[j + j * nb];
+      for (int k = 0; k < j; k++) d -= L[j + k * nb] * L[j + k * nb];
+      d = sqrt(fmax(d, 1e-300));
+      L[j + j * nb] = d;
+      for (int i = j + 1; i < nb; i++) {
+        double s = L[i + j * nb];
+        for (int k = 0; k < j; k++) s -= L[i + k * nb] * L[j + k * nb];
+        L[i + j * nb] = s / d;
+      }
+    }
+    // inverse of lower L (Li lower)
+    for (int j = 0; j < nb; j++) {
+      Li[j + j * nb] = 1.0 / L[j + j * nb];
+      for (int i = j + 1; i < nb; i++) {
+        double s = 0.0;
+        for (int k = j; k < i; k++) s += L[i + k * nb] * Li[k + j * nb];
+        Li[i + j * nb] = -s / L[i + i * nb];
+      }
+    }
+  }
+  __syncthreads();
+  // R = L^T upper, R^{-1} = (L^{-1})^T
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e % nb, j = e / nb;
+    Rinv[e] = Li[j + i * nb];
+  }
+}
+// Y <- Y R^{-1}  (row-parallel)
+__global__ void td_apply_rinv(double* Y, int64_t ldy, int nb, const double* Rinv, int64_t n) {
+  extern __shared__ double rs[];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) rs[e] = Rinv[e];
+  __syncthreads();
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double y[64];
+  for (int j = 0; j < nb; j++) y[j] = Y[SK_IDX(r, j, ldy)];
+  for (int j = 0; j < nb; j++) {
+    double s = 0.0;
+    for (int i = 0; i <= j; i++) s += y[i] * rs[i + j * nb];
+    Y[SK_IDX(r, j, ldy)] = s;
+  }
+}
+
+// D assembly (Algorithm 1 step 3; reading R1):
+// X[:, c] = Re(D q_c), X[:, nev + c] = Im(D q_c); row k: k%4 = 0 -> Re +q, 1 -> Im +q,
+// 2 -> Re -q, 3 -> Im -q.
+__global__ void assemble_D_kernel(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx) {
+  int64_t c = blockIdx.y;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    double q = Q[SK_IDX(k, c, ldq)];
+    double re = 0.0, im = 0.0;
+    switch (k & 3) {
+      case 0: re = q; break;
+      case 1: im = q; break;
+      case 2: re = -q; break;
+      default: im = -q; break;
+    }
+    X[SK_IDX(k, c, ldx)] = re;
+    X[SK_IDX(k, nev + c, ldx)] = im;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+static constexpr int kReorthNB = 32;
+static constexpr int64_t kGramRows = 1024;
+
+void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, int window) {
+  int64_t nn = std::max<int64_t>(n, 1);
+  w.a2 = ar.take<double>(nn);
+  w.lamc = ar.take<double>(nn);
+  w.tsk = ar.take<int64_t>(3 * nn);
+  if (!vectors) return;
+  int64_t ne = std::max<int64_t>(nev, 1);
+  w.lamv = ar.take<double>(ne);
+  w.gblk = ar.take<double>(ne);
+  w.vblk = ar.take<int64_t>(2 * ne);
+  // bound the interleaved LU workspace to ~1 GiB
+  int64_t batch = std::max<int64_t>(1, std::min<int64_t>(ne, (int64_t)(1ll << 30) / (41 * nn)));
+  w.batch = batch;
+  w.inv = ar.take<double>((size_t)5 * nn * batch);
+  w.inv_in = ar.take<unsigned char>((size_t)nn * batch);
+  w.nfail = ar.take<int>(1);
+  int64_t nchunks = (nn + kGramRows - 1) / kGramRows;
+  int p = window + kReorthNB;
+  w.part = ar.take<double>((size_t)nchunks * p * kReorthNB + (size_t)p * kReorthNB);
+  w.H = ar.take<double>((size_t)p * kReorthNB);
+  w.Rinv = ar.take<double>((size_t)kReorthNB * kReorthNB);
+}
+
+static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* Y, int64_t ldy, int nb, int64_t n,
+                                  TridWork& w, cudaStream_t st) {
+  int64_t nchunks = (n + kGramRows - 1) / kGramRows;
+  td_gram_partial<<<(unsigned)nchunks, 256, 0, st>>>(Qp, ldq, p, Y, ldy, nb, n, kGramRows, w.part);
+  int cnt = p * nb;
+  td_reduce_partials<<<(cnt + 255) / 256, 256, 0, st>>>(w.part, (int)nchunks, cnt, w.H);
+  return cudaGetLastError();
+}
+
+// lam (nev, descending, device out); Q (n x nev, ldq) or null.
+cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q, int64_t ldq,
+                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st) {
+  cudaError_t e;
+  *nfail_out = 0;
+  if (nev <= 0) return cudaSuccess;
+  // alpha to host (n-1 doubles): split points, Gershgorin bounds, task lists
+  std::vector<double> al(std::max<int64_t>(n - 1, 1), 0.0);
+  if (n > 1) {
+    e = cudaMemcpyAsync(al.data(), alpha_d, sizeof(double) * (n - 1), cudaMemcpyDeviceToHost, st);
+    if (e) return e;
+    e = cudaStreamSynchronize(st);
+    if (e) return e;
+  }
+  std::vector<int64_t> bs{0};
+  for (int64_t k = 0; k + 1 < n; k++) if (al[k] == 0.0) bs.push_back(k + 1);
+  bs.push_back(n);
+  const int64_t nblk = (int64_t)bs.size() - 1;
+  double amax2 = 1.0;
+  for (int64_t k = 0; k + 1 < n; k++) amax2 = std::max(amax2, al[k] * al[k]);
+  const double pivmin = DBL_MIN * amax2;
+  std::vector<double> a2(std::max<int64_t>(n, 1), 0.0);
+  for (int64_t k = 0; k + 1 < n; k++) a2[k] = al[k] * al[k];
+  std::vector<int64_t> ts0, tm, ti, tb;
+  std::vector<double> gb(nblk, 0.0);
+  for (int64_t b = 0; b < nblk; b++) {
+    int64_t s0 = bs[b], m = bs[b + 1] - bs[b];
+    double g = 0.0;
+    for (int64_t k = 0; k < m; k++) {
+      double r = (k > 0 ? std::fabs(al[s0 + k - 1]) : 0.0) + (k + 1 < m ? std::fabs(al[s0 + k]) : 0.0);
+      g = std::max(g, r);
+    }
+    gb[b] = g;
+    int64_t kb = std::min(m, nev);
+    for (int64_t i = 0; i < kb; i++) { ts0.push_back(s0); tm.push_back(m); ti.push_back(m - 1 - i); tb.push_back(b); }
+  }
+  const int64_t ntask = (int64_t)ts0.size();
+  // each unreduced block bisects inside its own Gershgorin interval
+  std::vector<double> lamc(ntask);
+  {
+    e = cudaMemcpyAsync(w.a2, a2.data(), sizeof(double) * std::max<int64_t>(n, 1), cudaMemcpyHostToDevice, st);
+    if (e) return e;
+    int64_t* d_s0 = w.tsk;
+    int64_t* d_m = w.tsk + n;
+    int64_t* d_i = w.tsk + 2 * n;
+    cudaMemcpyAsync(d_s0, ts0.data(), sizeof(int64_t) * ntask, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_m, tm.data(), sizeof(int64_t) * ntask, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_i, ti.data(), sizeof(int64_t) * ntask, cudaMemcpyHostToDevice, st);
+    // per-block g: launch per distinct block bound only when split (rare); common case one block
+    if (nblk == 1) {
+      td_bisect_kernel<<<(unsigned)((ntask + 127) / 128), 128, 0, st>>>(w.a2, d_s0, d_m, d_i, ntask, gb[0], pivmin,
+                                                                        w.lamc);
+    } else {
+      int64_t q0 = 0;
+      for (int64_t b = 0; b < nblk; b++) {
+        int64_t cnt = std::min(bs[b + 1] - bs[b], nev);
+        td_bisect_kernel<<<(unsigned)((cnt + 127) / 128), 128, 0, st>>>(w.a2, d_s0 + q0, d_m + q0, d_i + q0, cnt,
+                                                                         gb[b], pivmin, w.lamc + q0);
+        q0 += cnt;
+      }
+    }
+    e = cudaMemcpyAsync(lamc.data(), w.lamc, sizeof(double) * ntask, cudaMemcpyDeviceToHost, st);
+    if (e) return e;
+    e = cudaStreamSynchronize(st);
+    if (e) return e;
+  }
+  // stable selection of the nev largest (ties in block order)
+  std::vector<int64_t> ord(ntask);
+  for (int64_t i = 0; i < ntask; i++) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return lamc[x] > lamc[y]; });
+  std::vector<double> lam(nev);
+  for (int64_t i = 0; i < nev; i++) lam[i] = lamc[ord[i]];
+  e = cudaMemcpyAsync(lam_out, lam.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
+  if (e) return e;
+  if (!Q) return cudaStreamSynchronize(st);
+
+  // per-vector block info and perturbed eigenvalues (dstein: within a block, descending,
+  // lambda_k <- lambda_{k-1} - 10 eps g when closer)
+  std::vector<double> lv(nev), gv(nev);
+  std::vector<int64_t> vb(2 * nev);
+  std::vector<int64_t> last_in_blk(nblk, -1);
+  std::vector<double> last_lam(nblk, 0.0);
+  std::vector<int64_t> clus_start(nev, 0);
+  for (int64_t i = 0; i < nev; i++) {
+    int64_t b = tb[ord[i]];
+    double g = gb[b];
+    double x = lam[i];
+    if (last_in_blk[b] >= 0 && last_lam[b] - x < 10.0 * DBL_EPSILON * g) x = last_lam[b] - 10.0 * DBL_EPSILON * g;
+    last_lam[b] = x;
+    last_in_blk[b] = i;
+    lv[i] = x; gv[i] = g;
+    vb[i] = bs[b]; vb[nev + i] = bs[b + 1] - bs[b];
+  }
+  // clusters (global order): consecutive gap < 1e-6 * gmax
+  double gmax = 0.0;
+  for (double g : gb) gmax = std::max(gmax, g);
+  for (int64_t i = 1; i < nev; i++) clus_start[i] = (lam[i - 1] - lam[i] < 1e-6 * gmax) ? clus_start[i - 1] : i;
+  cudaMemcpyAsync(w.lamv, lv.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(w.gblk, gv.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(w.vblk, vb.data(), sizeof(int64_t) * 2 * nev, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(w.nfail, 0, sizeof(int), st);
+  for (int64_t c0 = 0; c0 < nev; c0 += w.batch) {
+    int64_t nb = std::min(w.batch, nev - c0);
+    InvArgs a;
+    a.alpha = alpha_d; a.vs0 = w.vblk; a.vm = w.vblk + nev; a.lam = w.lamv; a.gblk = w.gblk;
+    a.nvec = nb; a.col0 = c0; a.Q = Q; a.ldq = ldq; a.n = n;
+    size_t stride = (size_t)n * nb;
+    a.wa = w.inv; a.wb = w.inv + stride; a.wc = w.inv + 2 * stride; a.wd = w.inv + 3 * stride; a.y = w.inv + 4 * stride;
+    a.win = w.inv_in; a.seed = prm.seed; a.nfail = w.nfail;
+    td_inverse_kernel<<<(unsigned)((nb + 63) / 64), 64, 0, st>>>(a);
+  }
+  e = cudaGetLastError();
+  if (e) return e;
+  // re-orthogonalisation in blocks of 32 (descending order)
+  const int W = prm.reorth_w;
+  for (int64_t k0 = 0; k0 < nev; k0 += kReorthNB) {
+    int nb = (int)std::min<int64_t>(kReorthNB, nev - k0);
+    int64_t p0 = std::max<int64_t>(0, k0 - W);
+    int64_t cs = clus_start[k0];
+    if (cs < p0) p0 = cs;
+    double* Y = Q + SK_IDX(0, k0, ldq);
+    // CGS2 against [p0, k0) in chunks of <= 64 previous vectors
+    for (int pass = 0; pass < 2; pass++) {
+      for (int64_t q0 = p0; q0 < k0; q0 += 64) {
+        int p = (int)std::min<int64_t>(64, k0 - q0);
+        const double* Qp = Q + SK_IDX(0, q0, ldq);
+        e = reorth_project(Qp, ldq, p, Y, ldq, nb, n, w, st);
+        if (e) return e;
+        td_sub_proj<<<(unsigned)((n + 127) / 128), 128, (size_t)p * nb * 8, st>>>(Qp, ldq, p, w.H, Y, ldq, nb, n);
+      }
+    }
+    // CholQR2 within the block
+    if (nb > 1) {
+      for (int pass = 0; pass < 2; pass++) {
+        e = reorth_project(Y, ldq, nb, Y, ldq, nb, n, w, st);
+        if (e) return e;
+        td_chol_inv<<<1, 128, 0, st>>>(w.H, nb, w.Rinv);
+        td_apply_rinv<<<(unsigned)((n + 127) / 128), 128, (size_t)nb * nb * 8, st>>>(Y, ldq, nb, w.Rinv, n);
+      }
+    }
+  }
+  int nf = 0;
+  e = cudaMemcpyAsync(&nf, w.nfail, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e) return e;
+  e = cudaStreamSynchronize(st);
+  *nfail_out = nf;
+  return e;
+}
+
+cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st) {
+  if (nev <= 0) return cudaSuccess;
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)nev);
+  assemble_D_kernel<<<grid, 256, 0, st>>>(Q, ldq, n, nev, X, ldx);
+  return cudaGetLastError();
+}
+
+}  // namespace sk

@@ -1,0 +1,251 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle on identical
+seeded inputs (BASELINE north_star tolerances), plus kernel-level checks of each stage
+on shared inputs (SURVEY §4 tier 2).  Eigenvectors are compared by residual, unitarity
+and subspace angle -- never elementwise (phase / degeneracy, reading R7).
+
+Tolerances (BASELINE.json north_star):
+  eigenvalues     max |lam - lam_oracle|               <= 1e-12 * ||A||_F
+  residual        max_k ||A z_k - i lam_k z_k|| / (n ||A||_F) <= 1e-13
+  orthogonality   max |Z^H Z - I|                       <= 1e-11
+  subspace        sin angle(z_k, z_k_oracle) <= max(1e-9, 1e3 eps ||A||_2 / gap_k) for simple lam_k
+"""
+import numpy as np
+import pytest
+
+import oracle
+import skewgen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(float).eps
+
+
+@pytest.fixture(scope="module")
+def sk():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1912_04062_b200 as m
+    m.lib()
+    return m
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _check_pairs(A, lam, Zre, Zim, lam_ref, Zre_ref=None, Zim_ref=None):
+    n = A.shape[0]
+    nA = np.linalg.norm(A)
+    Z = Zre + 1j * Zim
+    assert np.all(np.diff(lam) <= 0), "descending"
+    err_l = np.max(np.abs(lam - lam_ref)) if len(lam) else 0.0
+    assert err_l <= 1e-12 * max(nA, 1e-300), f"eigenvalues {err_l / nA:.3e} x ||A||_F"
+    res = np.max(np.linalg.norm(A @ Z - Z * (1j * lam), axis=0)) / (n * nA)
+    assert res <= 1e-13, f"residual {res:.3e}"
+    orth = np.max(np.abs(Z.conj().T @ Z - np.eye(len(lam))))
+    assert orth <= 1e-11, f"orthogonality {orth:.3e}"
+    if Zre_ref is not None:
+        Zo = Zre_ref + 1j * Zim_ref
+        n2 = np.linalg.norm(A, 2)
+        full = np.concatenate([lam_ref, [-lam_ref[0]]]) if len(lam_ref) else lam_ref
+        for k in range(len(lam)):
+            others = np.delete(lam_ref, k)
+            gap = min(np.min(np.abs(others - lam_ref[k])) if len(others) else np.inf, 2 * lam_ref[k])
+            if gap < 1e-6 * n2:
+                continue   # cluster: covered by the subspace test below
+            zo = Zo[:, k] / np.linalg.norm(Zo[:, k])
+            z = Z[:, k] / np.linalg.norm(Z[:, k])
+            sin = np.linalg.norm(z - np.vdot(zo, z) * zo)     # cancellation-free sin of the angle
+            assert sin <= max(1e-9, 1e3 * EPS * n2 / gap), f"vector {k}: sin {sin:.3e} gap {gap:.3e}"
+    return dict(eig=err_l / max(nA, 1e-300), res=res, orth=orth)
+
+
+# ------------------------------------------------------------------ full solve (Algorithm 1)
+@pytest.mark.parametrize("n", [2, 3, 4, 64, 65, 66, 129, 256, 257, 513, 1024])
+def test_skew_eig_random_vs_oracle(sk, n):
+    A = skewgen.random_skew(n, n)
+    lam_o, Zre_o, Zim_o, st = oracle.skew_eig(A)
+    assert st == 0
+    lam, Zre, Zim = sk.skew_eig(_cuda(A))
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
+
+
+@pytest.mark.parametrize("nev", [1, 7, 100])
+def test_skew_eig_partial_spectrum(sk, nev):
+    n = 300
+    A = skewgen.random_skew(n, 77)
+    lam_o, Zre_o, Zim_o, _ = oracle.skew_eig(A, nev)
+    lam, Zre, Zim = sk.skew_eig(_cuda(A), nev)
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
+
+
+def test_skew_eig_2x2_closed_form(sk):
+    a = 1.7
+    A = np.array([[0.0, a], [-a, 0.0]])
+    lam, Zre, Zim = sk.skew_eig(_cuda(A))
+    z = Zre.cpu().numpy()[:, 0] + 1j * Zim.cpu().numpy()[:, 0]
+    assert abs(lam.item() - a) <= 4 * EPS * a
+    assert abs(abs(np.vdot(np.array([1, 1j]) / np.sqrt(2), z)) - 1) <= 8 * EPS
+
+
+def test_skew_eig_toeplitz_closed_form(sk):
+    n = 256
+    A = skewgen.skew_toeplitz(n)
+    lam, Zre, Zim = sk.skew_eig(_cuda(A))
+    exact = 2 * np.cos(np.arange(1, n // 2 + 1) * np.pi / (n + 1))
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), exact)
+
+
+def test_skew_eig_J_degenerate(sk):
+    n = 128
+    A = skewgen.J_matrix(n)
+    lam, Zre, Zim = sk.skew_eig(_cuda(A))
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), np.ones(n // 2))
+
+
+def test_skew_eig_planted_repeated(sk):
+    sig = np.repeat(np.array([3.0, 2.0, 1.0, 0.5]), 24)
+    A = skewgen.planted_skew(sig, seed=5)
+    lam, Zre, Zim = sk.skew_eig(_cuda(A))
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), np.sort(sig)[::-1])
+
+
+def test_skew_eig_zero_matrix(sk):
+    n = 70
+    A = np.zeros((n, n))
+    lam = sk.skew_eigvals(_cuda(A), 5)
+    assert np.all(lam.cpu().numpy() == 0.0)
+
+
+def test_skew_eigvals_matches_oracle(sk):
+    n = 700
+    A = skewgen.random_skew(n, 3)
+    lam_o, *_ = oracle.skew_eig(A, 200, want_vectors=False)
+    lam = sk.skew_eigvals(_cuda(A), 200).cpu().numpy()
+    assert np.max(np.abs(lam - lam_o)) <= 1e-12 * np.linalg.norm(A)
+
+
+def test_determinism_bitwise(sk):
+    A = skewgen.random_skew(300, 9)
+    l1, r1, i1 = sk.skew_eig(_cuda(A))
+    l2, r2, i2 = sk.skew_eig(_cuda(A))
+    assert torch.equal(l1, l2) and torch.equal(r1, r2) and torch.equal(i1, i2)
+
+
+def test_host_pointer_entry_matches_device(sk):
+    n, nev = 200, 100
+    A = skewgen.random_skew_lower_colmajor(n, 21)
+    lam = np.zeros(nev)
+    Zre = np.zeros((n, nev), order="F")
+    Zim = np.zeros((n, nev), order="F")
+    sk.skew_eig_host(A, nev, lam, Zre, Zim)
+    Afull = skewgen.random_skew(n, 21)
+    lam_o, Zre_o, Zim_o, _ = oracle.skew_eig(Afull)
+    _check_pairs(Afull, lam, Zre, Zim, lam_o, Zre_o, Zim_o)
+    # host A is not modified
+    assert np.array_equal(A, skewgen.random_skew_lower_colmajor(n, 21))
+
+
+def test_bad_arguments(sk):
+    import ctypes
+    L = sk.lib()
+    c = sk._ctx(None)
+    A = torch.zeros((8, 8), dtype=torch.float64, device="cuda")
+    lam = torch.zeros(8, dtype=torch.float64, device="cuda")
+    assert L.skew_eig(c.h, 8, ctypes.c_void_p(A.data_ptr()), 8, 5, ctypes.c_void_p(lam.data_ptr()),
+                      ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(A.data_ptr()), 8) == -5
+    assert L.skew_eig(c.h, 8, ctypes.c_void_p(A.data_ptr()), 4, 2, ctypes.c_void_p(lam.data_ptr()),
+                      ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(A.data_ptr()), 8) == -4
+    assert L.skew_eig(c.h, 0, None, 1, 1, None, None, None, 1) == -2
+
+
+# ------------------------------------------------------------------ stage checks (shared inputs)
+def _Q_band(V, T, npanel, b, n):
+    Q = np.eye(n)
+    for j in range(npanel):
+        Vj = V[:, j * b:(j + 1) * b]
+        Tj = T[:, j * b:(j + 1) * b]
+        Q = Q @ (np.eye(n) - Vj @ Tj @ Vj.T)
+    return Q
+
+
+@pytest.mark.parametrize("n", [66, 130, 257, 600])
+def test_reduce_to_band_similarity(sk, n):
+    A = skewgen.random_skew(n, 1000 + n)
+    Ab, V, T, tau, npanel = sk.reduce_to_band(_cuda(A))
+    b = sk.band_width()
+    Ab = Ab.cpu().numpy()
+    B = np.zeros((n, n))
+    for c in range(n):
+        for d in range(1, b + 1):
+            if c + d < n:
+                B[c + d, c] = Ab[c + d, c]
+    B = B - B.T
+    if npanel:
+        V = V.cpu().numpy()
+        T = T.cpu().numpy()
+        Q = _Q_band(V, T, npanel, b, n)
+        nA = np.linalg.norm(A)
+        assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 100 * n * EPS
+        assert np.linalg.norm(Q.T @ A @ Q - B) <= 50 * n * EPS * nA
+    ev = np.linalg.eigvalsh(-1j * B)
+    ref = np.linalg.eigvalsh(-1j * A)
+    assert np.max(np.abs(ev - ref)) <= 1e-12 * np.linalg.norm(A)
+
+
+@pytest.mark.parametrize("n,b", [(40, 8), (300, 64), (301, 17)])
+def test_band_to_tridiag_similarity(sk, n, b):
+    full = skewgen.random_skew(n, 5 * n + b)
+    B = np.zeros((n, n))
+    for i in range(n):
+        for j in range(n):
+            if abs(i - j) <= b:
+                B[i, j] = full[i, j]
+    ldab = b + 1
+    AB = np.zeros((ldab, n))
+    for c in range(n):
+        for d in range(b + 1):
+            if c + d < n:
+                AB[d, c] = B[c + d, c]
+    ABt = torch.from_numpy(AB.T.copy()).cuda().t()   # column-major (ldab, n)
+    X = torch.eye(n, dtype=torch.float64, device="cuda").t().contiguous().t()
+    alpha = sk.band_to_tridiag(ABt, b, X).cpu().numpy()
+    Q2 = X.cpu().numpy()
+    T = np.diag(-alpha, -1) + np.diag(alpha, 1)
+    assert np.linalg.norm(Q2.T @ Q2 - np.eye(n)) <= 100 * n * EPS
+    assert np.linalg.norm(Q2.T @ B @ Q2 - T) <= 50 * n * EPS * np.linalg.norm(B)
+
+
+@pytest.mark.parametrize("n", [10, 257, 2000])
+def test_tridiag_stage_vs_oracle(sk, n):
+    a = skewgen.uniform_pm1(np.arange(n - 1, dtype=np.uint64) + np.uint64(3 * n))
+    nev = n // 2
+    lam_o, Q_o, _ = oracle.tridiag_eig(a, nev)
+    lam, Q = sk.tridiag_eig(torch.from_numpy(a).cuda(), nev)
+    lam = lam.cpu().numpy()
+    Q = Q.cpu().numpy()
+    g = 2 * np.max(np.abs(a))
+    assert np.max(np.abs(lam - lam_o)) <= 100 * n * EPS * g
+    Tm = np.diag(a, 1) + np.diag(a, -1)
+    assert np.max(np.linalg.norm(Tm @ Q - Q * lam, axis=0)) <= 50 * n * EPS * g
+    assert np.max(np.abs(Q.T @ Q - np.eye(nev))) <= 1e-11
+
+
+# ------------------------------------------------------------------ BSE entry point
+@pytest.mark.parametrize("n", [2, 64, 256])
+def test_bse_vs_oracle(sk, n):
+    M = skewgen.bse_spd(n, 10000 + n)
+    lam_o, Zre_o, Zim_o, st, piv, L = oracle.bse_eig(M)
+    assert st == 0
+    lam, Zre, Zim = sk.skew_eig_bse(_cuda(M))
+    W = oracle.form_W(L)
+    W = W - W.T
+    _check_pairs(W, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o)
+
+
+def test_bse_not_definite(sk):
+    M = np.array([[1.0, -1.0], [-1.0, 1.0]])
+    with pytest.raises(sk.SkewError) as ei:
+        sk.skew_eig_bse(_cuda(M))
+    assert ei.value.status == 4 and ei.value.pivot == 2
