@@ -87,6 +87,14 @@ int skew_set_workspace(skew_ctx ctx, void* dptr, size_t bytes);
 int skew_eig(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev,
              double* lambda, double* Zre, double* Zim, int64_t ldz);
 
+/* Same solve, eigenvectors of the index range [k0, k1) only (0 <= k0 < k1 <= nev):
+ * lambda receives all nev eigenvalues, Zre/Zim (n x (k1-k0), ldz) the vectors
+ * z_{k0} .. z_{k1-1}.  This is the per-rank call of the multi-GPU path (DESIGN.md
+ * "Multi-GPU": each rank owns a contiguous eigenpair range; the back-transforms of
+ * different ranges are independent). */
+int skew_eig_range(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, int64_t k0, int64_t k1,
+                   double* lambda, double* Zre, double* Zim, int64_t ldz);
+
 /* Eigenvalues only (Algorithm 1 steps 1-2): the nev largest lambda_k, descending. */
 int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda);
 

@@ -37,6 +37,16 @@ int skew_stage_band_to_tridiag(skew_ctx ctx, int64_t n, int b, const double* AB,
 int skew_stage_tridiag_eig(skew_ctx ctx, int64_t n, const double* alpha, int64_t nev,
                            double* lambda, double* Q, int64_t ldq);
 
+/* Kernel accounting for measurement.  Every kernel launch of the library belongs to
+ * one of SKEW_KERNEL_CLASSES classes (skew_kernel_class_name); skew_kernel_stats
+ * returns, for the last call, the number of launches per class and -- when
+ * profiling is on -- the summed device time (ms) of each class measured with CUDA
+ * events recorded on the context stream around the launches. */
+#define SKEW_KERNEL_CLASSES 18
+int skew_set_profiling(skew_ctx ctx, int on);
+int skew_kernel_stats(skew_ctx ctx, double* ms_out, int64_t* launches_out, int count);
+const char* skew_kernel_class_name(int cls);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,7 @@ column-major layout the C-ABI takes).
 import ctypes
 import os
 
-__all__ = ["lib", "Context", "skew_eig", "skew_eigvals", "skew_eig_bse", "skew_eig_host",
+__all__ = ["lib", "Context", "skew_eig", "skew_eig_range", "skew_eig_host_range", "skew_eigvals", "skew_eig_bse", "skew_eig_host",
            "reduce_to_band", "band_to_tridiag", "tridiag_eig", "expand_half_spectrum", "SkewError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -40,6 +40,7 @@ EXPORTS = {
     "skew_set_workspace": ([_vp, _vp, ctypes.c_size_t], ctypes.c_int),
     "skew_eig": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
     "skew_eigvals": ([_vp, _i64, _dp, _i64, _i64, _dp], ctypes.c_int),
+    "skew_eig_range": ([_vp, _i64, _dp, _i64, _i64, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
     "skew_eig_bse": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64, ctypes.POINTER(_i64)], ctypes.c_int),
     "skew_stage_times": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int], ctypes.c_int),
     "skew_last_nfail": ([_vp], _i64),
@@ -48,7 +49,11 @@ EXPORTS = {
     "skew_stage_reduce_to_band": ([_vp, _i64, _dp, _i64, _dp, _i64, _dp, _dp, ctypes.POINTER(_i64)], ctypes.c_int),
     "skew_stage_band_to_tridiag": ([_vp, _i64, ctypes.c_int, _dp, _i64, _dp, _dp, _i64, _i64], ctypes.c_int),
     "skew_stage_tridiag_eig": ([_vp, _i64, _dp, _i64, _dp, _dp, _i64], ctypes.c_int),
+    "skew_set_profiling": ([_vp, ctypes.c_int], ctypes.c_int),
+    "skew_kernel_stats": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), ctypes.c_int], ctypes.c_int),
+    "skew_kernel_class_name": ([ctypes.c_int], ctypes.c_char_p),
 }
+KERNEL_CLASSES = 18
 
 STAGES = ["f2b", "b2t", "tridiag", "bt2", "bt1", "output", "bse"]
 
@@ -125,6 +130,16 @@ class Context:
         lib().skew_stage_times(self.h, arr, 7)
         return dict(zip(STAGES, list(arr)))
 
+    def set_profiling(self, on=True):
+        self._check(lib().skew_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_stats(self):
+        """{class: (ms, launches)} for the last call (ms only when profiling is on)."""
+        ms = (ctypes.c_double * KERNEL_CLASSES)()
+        la = (_i64 * KERNEL_CLASSES)()
+        lib().skew_kernel_stats(self.h, ms, la, KERNEL_CLASSES)
+        return {lib().skew_kernel_class_name(i).decode(): (ms[i], la[i]) for i in range(KERNEL_CLASSES)}
+
     def last_error(self):
         return lib().skew_last_error(self.h).decode()
 
@@ -175,6 +190,38 @@ def skew_eig(A, nev=None, ctx=None, overwrite_a=False):
                         _dp(Zim.data_ptr()), Zre.stride(1))
     c._check(rc, allow=(SKEW_ERR_NOCONV,))
     return lam[:nev], Zre[:, :nev], Zim[:, :nev]
+
+
+def skew_eig_range(A, nev, k0, k1, ctx=None, overwrite_a=False):
+    """All nev eigenvalues and the eigenvectors of the index range [k0, k1) (multi-GPU
+    per-rank call).  Returns (lam (nev,), Zre (n, k1-k0), Zim (n, k1-k0))."""
+    torch = _torch()
+    c = _ctx(ctx)
+    n = A.shape[0]
+    Ac = A if (overwrite_a and A.stride(0) == 1) else _colmajor(torch, A.to(device=c.device, dtype=torch.float64))
+    c.ensure_workspace(n, nev, SKEW_WS_VECTORS)
+    lam = torch.empty(max(nev, 1), dtype=torch.float64, device=c.device)
+    m = max(k1 - k0, 1)
+    Zre = _new_colmajor(torch, n, m, c.device)
+    Zim = _new_colmajor(torch, n, m, c.device)
+    rc = lib().skew_eig_range(c.h, n, _dp(Ac.data_ptr()), Ac.stride(1), nev, k0, k1, _dp(lam.data_ptr()),
+                              _dp(Zre.data_ptr()), _dp(Zim.data_ptr()), Zre.stride(1))
+    c._check(rc, allow=(SKEW_ERR_NOCONV,))
+    return lam[:nev], Zre[:, :k1 - k0], Zim[:, :k1 - k0]
+
+
+def skew_eig_host_range(A_host, nev, k0, k1, lam_host, Zre_host, Zim_host, ctx=None):
+    """skew_eig_range with HOST buffers (column-major, ld = n): end-to-end entry."""
+    c = _ctx(ctx)
+    n = A_host.shape[0]
+    c.ensure_workspace(n, nev, SKEW_WS_VECTORS | SKEW_WS_HOST_STAGING)
+
+    def ptr(x):
+        return x.ctypes.data if hasattr(x, "ctypes") else x.data_ptr()
+    rc = lib().skew_eig_range(c.h, n, _dp(ptr(A_host)), n, nev, k0, k1, _dp(ptr(lam_host)), _dp(ptr(Zre_host)),
+                              _dp(ptr(Zim_host)), n)
+    c._check(rc, allow=(SKEW_ERR_NOCONV,))
+    return rc
 
 
 def skew_eigvals(A, nev=None, ctx=None):

@@ -14,6 +14,8 @@
 
 namespace sk {
 
+thread_local Prof* g_prof = nullptr;
+
 // ------------------------------------------------------------------------------------
 struct Plan {
   F2BLayout f2b;
@@ -88,6 +90,7 @@ using namespace sk;
 
 struct skew_ctx_s {
   Ctx c;
+  Prof prof;
   cudaEvent_t ev_start[ST_COUNT];
   cudaEvent_t ev_stop[ST_COUNT];
   bool used[ST_COUNT];
@@ -114,7 +117,18 @@ static void tcollect(skew_ctx ctx) {
     else ctx->c.stage_ms[s] = 0.0;
   }
 }
-static void treset(skew_ctx ctx) { for (int s = 0; s < ST_COUNT; s++) ctx->used[s] = false; }
+static void treset(skew_ctx ctx) {
+  for (int s = 0; s < ST_COUNT; s++) ctx->used[s] = false;
+  ctx->prof.reset();
+  g_prof = &ctx->prof;
+}
+// collect per-kernel-class event timings once the stream is synchronised
+static void kcollect(skew_ctx ctx) {
+  if (ctx->prof.on) ctx->prof.collect();
+}
+static const char* kNames[KC_COUNT] = {"panel_qr", "vt", "skew_symm", "w_correction", "skew_r2k", "band_extract",
+                                       "bulge_chase", "bisection", "inverse_iteration", "reorth", "assemble_D",
+                                       "bt2_tbuild", "bt2_apply", "bt1_prep", "bt1_z", "bt1_update", "output", "bse"};
 
 extern "C" {
 
@@ -180,6 +194,24 @@ int skew_stage_times(skew_ctx ctx, double* ms_out, int count) {
   return SKEW_OK;
 }
 
+int skew_set_profiling(skew_ctx ctx, int on) {
+  if (!ctx) return -1;
+  ctx->prof.on = (on != 0);
+  return SKEW_OK;
+}
+
+int skew_kernel_stats(skew_ctx ctx, double* ms_out, int64_t* launches_out, int count) {
+  if (!ctx) return -1;
+  if (count < 0 || count > KC_COUNT) return -4;
+  for (int i = 0; i < count; i++) {
+    if (ms_out) ms_out[i] = ctx->prof.ms[i];
+    if (launches_out) launches_out[i] = ctx->prof.launches[i];
+  }
+  return SKEW_OK;
+}
+
+const char* skew_kernel_class_name(int cls) { return (cls >= 0 && cls < KC_COUNT) ? kNames[cls] : "?"; }
+
 int64_t skew_last_nfail(skew_ctx ctx) { return ctx ? ctx->c.last_nfail : -1; }
 
 const char* skew_last_error(skew_ctx ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
@@ -201,7 +233,8 @@ const char* skew_status_string(int status) {
 // The solve driver shared by skew_eig / skew_eigvals / skew_eig_bse.
 // A_d: device skew input (strictly lower), destroyed.  lam_out/Zre/Zim: device or host.
 static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t nev, double* lambda, bool lam_host,
-                      double* Zre, double* Zim, int64_t ldz, bool z_host) {
+                      double* Zre, double* Zim, int64_t ldz, bool z_host, int64_t k0, int64_t k1) {
+  const int64_t nloc = k1 - k0;   // eigenvectors [k0, k1) are computed and returned
   Ctx& c = ctx->c;
   cudaStream_t st = c.stream;
   const int64_t n = p.n;
@@ -223,16 +256,18 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   // ---- tridiagonal eigenproblem
   tstart(ctx, ST_TRID);
   int64_t nfail = 0;
-  CK(trid_run(n, p.alpha, nev, p.lam, vec ? p.Q : nullptr, p.ldn, p.tw, c.prm, &nfail, st), "tridiagonal");
+  int64_t vlo = k0;
+  CK(trid_run(n, p.alpha, nev, p.lam, vec ? p.Q : nullptr, p.ldn, p.tw, c.prm, &nfail, st, k0, k1, &vlo),
+     "tridiagonal");
   c.last_nfail = nfail;
-  if (vec) CK(assemble_D(p.Q, p.ldn, n, nev, p.X, p.ldn, st), "assemble D");
+  if (vec) CK(assemble_D(p.Q + SK_IDX(0, k0 - vlo, p.ldn), p.ldn, n, nloc, p.X, p.ldn, st), "assemble D");
   tstop(ctx, ST_TRID);
   if (vec) {
     tstart(ctx, ST_BT2);
-    CK(bt2_run(p.b2t, p.bw, p.X, p.ldn, 2 * nev, st), "bt2");
+    CK(bt2_run(p.b2t, p.bw, p.X, p.ldn, 2 * nloc, st), "bt2");
     tstop(ctx, ST_BT2);
     tstart(ctx, ST_BT1);
-    if (p.f2b.npanel > 0) CK(bt1_run(p.f2b, p.vstore, p.fw.tau, p.X, p.ldn, 2 * nev, p.b1, st), "bt1");
+    if (p.f2b.npanel > 0) CK(bt1_run(p.f2b, p.vstore, p.fw.tau, p.X, p.ldn, 2 * nloc, p.b1, st), "bt1");
     tstop(ctx, ST_BT1);
   }
   // ---- output
@@ -241,39 +276,43 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
                      st), "lambda out");
   if (vec) {
     if (z_host) {
-      CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nev, cudaMemcpyDeviceToHost, st), "Zre out");
-      CK(cudaMemcpy2DAsync(Zim, ldz * 8, p.X + (size_t)p.ldn * nev, p.ldn * 8, n * 8, nev, cudaMemcpyDeviceToHost, st),
-         "Zim out");
+      CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost, st), "Zre out");
+      CK(cudaMemcpy2DAsync(Zim, ldz * 8, p.X + (size_t)p.ldn * nloc, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost,
+                           st), "Zim out");
     } else {
-      CK(split_output(p.X, p.ldn, n, nev, Zre, Zim, ldz, st), "split output");
+      CK(split_output(p.X, p.ldn, n, nloc, Zre, Zim, ldz, st), "split output");
     }
   }
   tstop(ctx, ST_OUT);
   CK(cudaStreamSynchronize(st), "sync");
   tcollect(ctx);
+  kcollect(ctx);
   return nfail > 0 ? SKEW_ERR_NOCONV : SKEW_OK;
 }
 
 static int eig_entry(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda, double* Zre,
-                     double* Zim, int64_t ldz, bool need_vec) {
+                     double* Zim, int64_t ldz, bool need_vec, int64_t k0, int64_t k1, int k0arg) {
   if (!ctx) return -1;
   if (n < 1) return -2;
   if (!A) return -3;
   if (lda < n) return -4;
   if (nev < 1 || nev > n / 2) return -5;
-  if (!lambda) return -6;
-  if (need_vec && !Zre) return -7;
-  if (need_vec && !Zim) return -8;
+  if (k0arg && (k0 < 0 || k0 >= nev)) return -k0arg;
+  if (k0arg && (k1 <= k0 || k1 > nev)) return -(k0arg + 1);
+  const int sh = k0arg ? 2 : 0;   // skew_eig_range has two more arguments before lambda
+  if (!lambda) return -(6 + sh);
+  if (need_vec && !Zre) return -(7 + sh);
+  if (need_vec && !Zim) return -(8 + sh);
   const bool vec = (Zre != nullptr || Zim != nullptr);
-  if (vec && (!Zre)) return -7;
-  if (vec && (!Zim)) return -8;
-  if (vec && ldz < n) return -9;
+  if (vec && (!Zre)) return -(7 + sh);
+  if (vec && (!Zim)) return -(8 + sh);
+  if (vec && ldz < n) return -(9 + sh);
   CK(cudaSetDevice(ctx->c.device), "set device");
   treset(ctx);
   const bool a_dev = is_device_ptr(A);
   const bool l_dev = is_device_ptr(lambda);
   const bool z_dev = vec ? is_device_ptr(Zre) : a_dev;
-  if (vec && is_device_ptr(Zim) != z_dev) return -8;
+  if (vec && is_device_ptr(Zim) != z_dev) return -(8 + sh);
   int flags = (vec ? SKEW_WS_VECTORS : 0) | (a_dev ? 0 : SKEW_WS_HOST_STAGING);
   Plan p;
   if (!ctx->c.ws || !plan_bind(ctx->c, p, n, nev, flags)) {
@@ -288,16 +327,21 @@ static int eig_entry(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t ne
     CK(cudaMemcpy2DAsync(p.Astage, ldad * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, ctx->c.stream), "A in");
     A_d = p.Astage;
   }
-  return solve_core(ctx, p, A_d, ldad, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev);
+  return solve_core(ctx, p, A_d, ldad, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev, k0, k1);
 }
 
 int skew_eig(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda, double* Zre, double* Zim,
              int64_t ldz) {
-  return eig_entry(ctx, n, A, lda, nev, lambda, Zre, Zim, ldz, true);
+  return eig_entry(ctx, n, A, lda, nev, lambda, Zre, Zim, ldz, true, 0, nev, 0);
+}
+
+int skew_eig_range(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, int64_t k0, int64_t k1,
+                   double* lambda, double* Zre, double* Zim, int64_t ldz) {
+  return eig_entry(ctx, n, A, lda, nev, lambda, Zre, Zim, ldz, true, k0, k1, 6);
 }
 
 int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda) {
-  return eig_entry(ctx, n, A, lda, nev, lambda, nullptr, nullptr, n, false);
+  return eig_entry(ctx, n, A, lda, nev, lambda, nullptr, nullptr, n, false, 0, nev, 0);
 }
 
 int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, double* lambda, double* Zre,
@@ -345,7 +389,8 @@ int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, d
     if (pivot_out) *pivot_out = piv;
     return SKEW_ERR_NOT_DEFINITE;
   }
-  int rc = solve_core(ctx, p, p.Astage, p.ldn, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev);
+  int rc = solve_core(ctx, p, p.Astage, p.ldn, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev, 0,
+                      nev);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev_start[ST_BSE], ctx->ev_stop[ST_BSE]);
   ctx->c.stage_ms[ST_BSE] = ms;
@@ -387,6 +432,7 @@ int skew_stage_reduce_to_band(skew_ctx ctx, int64_t n, double* A, int64_t lda, d
   }
   CK(cudaStreamSynchronize(st), "sync");
   tcollect(ctx);
+  kcollect(ctx);
   return SKEW_OK;
 }
 
@@ -419,6 +465,7 @@ int skew_stage_band_to_tridiag(skew_ctx ctx, int64_t n, int b, const double* AB,
   }
   CK(cudaStreamSynchronize(st), "sync");
   tcollect(ctx);
+  kcollect(ctx);
   return SKEW_OK;
 }
 
@@ -445,11 +492,12 @@ int skew_stage_tridiag_eig(skew_ctx ctx, int64_t n, const double* alpha, int64_t
   cudaStream_t st = ctx->c.stream;
   tstart(ctx, ST_TRID);
   int64_t nfail = 0;
-  CK(trid_run(n, alpha, nev, lam_d, Q, ldq, tw, ctx->c.prm, &nfail, st), "tridiagonal");
+  CK(trid_run(n, alpha, nev, lam_d, Q, ldq, tw, ctx->c.prm, &nfail, st, 0, nev, nullptr), "tridiagonal");
   tstop(ctx, ST_TRID);
   CK(cudaMemcpyAsync(lambda, lam_d, sizeof(double) * nev, cudaMemcpyDefault, st), "lambda");
   CK(cudaStreamSynchronize(st), "sync");
   tcollect(ctx);
+  kcollect(ctx);
   ctx->c.last_nfail = nfail;
   return nfail ? SKEW_ERR_NOCONV : SKEW_OK;
 }

@@ -349,10 +349,12 @@ void B2TLayout::init(int64_t n_, int b_, int k2_) {
 }
 
 cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st) {
+  KScope ks(KC_BAND, st);
   band_extract_kernel<<<(unsigned)std::max<int64_t>(n, 1), 128, 0, st>>>(A, lda, n, b, AB, ldab);
   return cudaGetLastError();
 }
 cudaError_t band_copy(const double* ABin, int64_t ldin, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st) {
+  KScope ks(KC_BAND, st);
   band_copy_kernel<<<(unsigned)std::max<int64_t>(n, 1), 128, 0, st>>>(ABin, ldin, n, b, AB, ldab);
   return cudaGetLastError();
 }
@@ -378,6 +380,7 @@ static int chase_grid(int64_t n, int b, int nsm) {
 cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cudaStream_t st) {
   cudaError_t e;
   const int64_t n = L.n;
+  KScope ks(KC_CHASE, st, n > 2 ? 2 : 1);
   if (n >= 2) {
     if (L.nblk > 0) {
       e = cudaMemcpyAsync(w.gofs, L.gofs.data(), sizeof(int64_t) * L.nblk, cudaMemcpyHostToDevice, st);
@@ -409,8 +412,11 @@ cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int6
   if (L.n <= 2 || L.ngroups == 0 || ncols == 0) return cudaSuccess;
   cudaError_t e;
   const int k2 = L.k2, b = L.b;
+  {
+  KScope ks(KC_BT2_T, st);
   bt2_tbuild_kernel<<<(unsigned)std::min<int64_t>(L.ngroups, 4096), 128, (size_t)(k2 * k2 + k2 * b) * 8, st>>>(
       w.qv, w.qtau, L.ngroups, k2, b, w.qT);
+  }
   constexpr int NB = 64, K2 = 32, MAXROWS = 96;
   if (k2 != K2 || b + k2 - 1 > MAXROWS) return cudaErrorInvalidValue;
   size_t smem = (size_t)(K2 * (MAXROWS + 4) + K2 * K2 + NB * (MAXROWS + 4) + 2 * NB * (K2 + 4)) * 8;
@@ -420,6 +426,7 @@ cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int6
     if (e) return e;
     set = true;
   }
+  KScope ks(KC_BT2, st);
   bt2_apply_kernel<NB, K2, MAXROWS><<<(unsigned)((ncols + NB - 1) / NB), 256, smem, st>>>(X, ldx, ncols, L.n, b, w.qv,
                                                                                          w.qT, w.gofs, L.nblk);
   return cudaGetLastError();

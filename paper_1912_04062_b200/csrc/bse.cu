@@ -104,6 +104,8 @@ __global__ void w11_kernel(const double* S, int64_t lds, int64_t m, double* W, i
 cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw, double* S, int64_t lds,
                       double* scratch, int64_t* status_d, cudaStream_t st) {
   cudaError_t e;
+  const int64_t nbl = (n + kCholNB - 1) / kCholNB;
+  KScope ks(KC_BSE, st, (int)(1 + nbl + 2 * (nbl - 1) + 4));
   cudaMemsetAsync(status_d, 0, sizeof(int64_t), st);
   diag_max_kernel<<<1, 256, 0, st>>>(M, ldm, n, scratch);
   for (int64_t j0 = 0; j0 < n; j0 += kCholNB) {

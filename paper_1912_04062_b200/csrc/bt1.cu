@@ -54,16 +54,18 @@ cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_
     const int64_t ldv = L.gld[g];
     // Gram G = V^T V
     {
+      KScope ks(KC_BT1_PREP, st, 3);
       GemmArgs ga;
       ga.M = K; ga.N = K; ga.K = m;
       ga.A = V; ga.lda = ldv; ga.B = V; ga.ldb = ldv; ga.C = w.G; ga.ldc = K; ga.alpha = 1.0; ga.beta = 0.0;
       e = gemm_dmma<64, 64, 16, 32, 16, 4, true, false, false>(ga, st);
       if (e) return e;
+      bt1_tbuild_kernel<<<(K + 63) / 64, 64, 0, st>>>(w.G, K, tau_all + j0 * b, w.T);
     }
-    bt1_tbuild_kernel<<<(K + 63) / 64, 64, 0, st>>>(w.G, K, tau_all + j0 * b, w.T);
     // U = V T^T
     const int64_t ldu = (m + 1) & ~int64_t(1);
     {
+      KScope ks(KC_BT1_PREP, st, 0);
       GemmArgs ga;
       ga.M = m; ga.N = K; ga.K = K;
       ga.A = V; ga.lda = ldv; ga.B = w.T; ga.ldb = K; ga.C = w.U; ga.ldc = ldu; ga.alpha = 1.0; ga.beta = 0.0;
@@ -73,6 +75,7 @@ cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_
     // Z = U^T X[r0:, :]
     double* Xr = X + r0;
     {
+      KScope ks(KC_BT1_Z, st);
       GemmArgs ga;
       ga.M = K; ga.N = ncols; ga.K = m;
       ga.A = w.U; ga.lda = ldu; ga.B = Xr; ga.ldb = ldx; ga.C = w.Z; ga.ldc = K; ga.alpha = 1.0; ga.beta = 0.0;
@@ -81,6 +84,7 @@ cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_
     }
     // X[r0:, :] -= V Z
     {
+      KScope ks(KC_BT1_UPD, st);
       GemmArgs ga;
       ga.M = m; ga.N = ncols; ga.K = K;
       ga.A = V; ga.lda = ldv; ga.B = w.Z; ga.ldb = K; ga.C = Xr; ga.ldc = ldx; ga.alpha = -1.0; ga.beta = 1.0;
@@ -105,6 +109,7 @@ cudaError_t split_output(const double* X, int64_t ldx, int64_t n, int64_t nev, d
                          cudaStream_t st) {
   if (nev <= 0) return cudaSuccess;
   dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)nev);
+  KScope ks(KC_OUT, st);
   split_output_kernel<<<grid, 256, 0, st>>>(X, ldx, n, nev, Zre, Zim, ldz);
   return cudaGetLastError();
 }

@@ -455,6 +455,7 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   a.smem_rows = use_smem ? (int)a.R : 0;
   void* args[] = {&a};
   cudaError_t e;
+  KScope ks(KC_PANEL, st);
   if (use_smem) {
     static bool set = false;
     if (!set) {
@@ -481,7 +482,10 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
   double* S = A + SK_IDX(r0, r0, lda);
   cudaError_t e;
   // U = V T
-  vt_kernel<<<(unsigned)((m + 127) / 128), 128, b * b * sizeof(double), st>>>(Vj, ldv, Tj, b, m, b, w.U, ldn);
+  {
+    KScope ks(KC_VT, st);
+    vt_kernel<<<(unsigned)((m + 127) / 128), 128, b * b * sizeof(double), st>>>(Vj, ldv, Tj, b, m, b, w.U, ldn);
+  }
   // X = S U
   {
     SymmArgs s;
@@ -497,19 +501,26 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
       if (e) return e;
       set = true;
     }
+    KScope ks(KC_SYMM, st);
     symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)((m + kSymmBM - 1) / kSymmBM), 256, smem, st>>>(s);
   }
   // W correction
   int nblk = (int)((m + kWRows - 1) / kWRows);
+  {
+  KScope ks(KC_WCORR, st, 3);
   vtx_partial_kernel<<<nblk, 256, 0, st>>>(Vj, ldv, w.X, ldn, m, b, kWRows, w.zpart);
   mb_kernel<<<1, 256, b * b * sizeof(double), st>>>(w.zpart, nblk, Tj, b, b, w.Mb);
   w_build_kernel<<<(unsigned)((m + 127) / 128), 128, b * b * sizeof(double), st>>>(Vj, ldv, w.X, ldn, w.Mb, m, b,
                                                                                      w.P, w.Q, ldn);
+  }
   // S_lower += P Q^T
   GemmArgs ga;
   ga.M = m; ga.N = m; ga.K = 2 * b;
   ga.A = w.P; ga.lda = ldn; ga.B = w.Q; ga.ldb = ldn; ga.C = S; ga.ldc = lda; ga.alpha = 1.0; ga.beta = 1.0;
-  e = gemm_dmma<128, 128, 16, 64, 32, 4, false, true, true>(ga, st);
+  {
+    KScope ks(KC_R2K, st);
+    e = gemm_dmma<128, 128, 16, 64, 32, 4, false, true, true>(ga, st);
+  }
   if (e) return e;
   return cudaGetLastError();
 }

@@ -67,6 +67,56 @@ struct F2BLayout {
 };
 
 
+// ---------------------------------------------------------------- kernel accounting
+// Every kernel launch of the library sits inside a KScope: it counts launches per
+// kernel class and, when profiling is on, brackets them with CUDA events on the
+// launching stream (skew_kernel_stats).
+enum KClass {
+  KC_PANEL = 0, KC_VT, KC_SYMM, KC_WCORR, KC_R2K, KC_BAND, KC_CHASE, KC_TRID_BISECT, KC_TRID_INV, KC_TRID_REORTH,
+  KC_ASSEMBLE, KC_BT2_T, KC_BT2, KC_BT1_PREP, KC_BT1_Z, KC_BT1_UPD, KC_OUT, KC_BSE, KC_COUNT
+};
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, size_t>> rec;   // (class, index of start event; stop = +1)
+  int64_t launches[KC_COUNT] = {};
+  double ms[KC_COUNT] = {};
+  void reset() { used = 0; rec.clear(); for (int i = 0; i < KC_COUNT; i++) { launches[i] = 0; ms[i] = 0.0; } }
+  cudaEvent_t ev() {
+    if (used == pool.size()) { cudaEvent_t e; cudaEventCreate(&e); pool.push_back(e); }
+    return pool[used++];
+  }
+  void collect() {
+    for (auto& r : rec) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, pool[r.second], pool[r.second + 1]) == cudaSuccess) ms[r.first] += t;
+    }
+    rec.clear();
+    used = 0;
+  }
+};
+extern thread_local Prof* g_prof;
+struct KScope {
+  int cls; cudaStream_t st; size_t idx = (size_t)-1;
+  KScope(int c, cudaStream_t s, int nlaunch = 1) : cls(c), st(s) {
+    if (!g_prof) return;
+    g_prof->launches[c] += nlaunch;
+    if (g_prof->on) {
+      cudaEvent_t a = g_prof->ev();
+      idx = g_prof->used - 1;
+      g_prof->ev();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~KScope() {
+    if (g_prof && g_prof->on && idx != (size_t)-1) {
+      cudaEventRecord(g_prof->pool[idx + 1], st);
+      g_prof->rec.push_back({cls, idx});
+    }
+  }
+};
+
 // ---------------------------------------------------------------- per-stage work buffers
 struct F2BWork {
   double* tau = nullptr;     // npanel * b
@@ -134,8 +184,10 @@ cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double*
 cudaError_t band_copy(const double* ABin, int64_t ldin, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st);
 // tridiag.cu
 void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, int window);
+// vectors of the global eigenpair range [k0, k1) (plus ghosts [vlo, k0)) go to Q columns 0..k1-vlo-1
 cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q, int64_t ldq,
-                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st);
+                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st, int64_t k0, int64_t k1,
+                     int64_t* vlo_out);
 cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st);
 // bt1.cu
 void bt1_reserve(Arena& ar, int64_t n, int64_t ncols, int K, BT1Work& w);

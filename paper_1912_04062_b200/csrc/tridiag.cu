@@ -64,7 +64,8 @@ struct InvArgs {
   const int64_t* vs0; const int64_t* vm;   // block start / size per vector
   const double* lam;            // perturbed eigenvalue per vector
   const double* gblk;           // block Gershgorin bound per vector
-  int64_t nvec; int64_t col0;   // vectors [col0, col0+nvec) of the output
+  int64_t nvec; int64_t col0;   // vectors [col0, col0+nvec) (global eigenpair indices)
+  int64_t qoff;                 // Q column of global index g is g - qoff
   double* Q; int64_t ldq; int64_t n;
   double *wa, *wb, *wc, *wd; unsigned char* win;   // [mmax][nvec]
   double* y;                    // [mmax][nvec]
@@ -85,7 +86,7 @@ __global__ void td_inverse_kernel(InvArgs a) {
   const double g = a.gblk[gv];
   const double eps = DBL_EPSILON;
   if (m == 1) {
-    for (int64_t i = 0; i < a.n; i++) a.Q[SK_IDX(i, gv, a.ldq)] = (i == s0) ? 1.0 : 0.0;
+    for (int64_t i = 0; i < a.n; i++) a.Q[SK_IDX(i, gv - a.qoff, a.ldq)] = (i == s0) ? 1.0 : 0.0;
     return;
   }
   // dlagtf: LU of T - lambda I with partial pivoting
@@ -187,7 +188,7 @@ __global__ void td_inverse_kernel(InvArgs a) {
   if (AT(y, jmax) < 0) scl = -scl;
   for (int64_t i = 0; i < a.n; i++) {
     double v = (i >= s0 && i < s0 + m) ? AT(y, i - s0) * scl : 0.0;
-    a.Q[SK_IDX(i, gv, a.ldq)] = v;
+    a.Q[SK_IDX(i, gv - a.qoff, a.ldq)] = v;
   }
 #undef AT
 }
@@ -330,6 +331,7 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
 static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* Y, int64_t ldy, int nb, int64_t n,
                                   TridWork& w, cudaStream_t st) {
   int64_t nchunks = (n + kGramRows - 1) / kGramRows;
+  KScope ks(KC_TRID_REORTH, st, 2);
   td_gram_partial<<<(unsigned)nchunks, 256, 0, st>>>(Qp, ldq, p, Y, ldy, nb, n, kGramRows, w.part);
   int cnt = p * nb;
   td_reduce_partials<<<(cnt + 255) / 256, 256, 0, st>>>(w.part, (int)nchunks, cnt, w.H);
@@ -338,7 +340,8 @@ static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* 
 
 // lam (nev, descending, device out); Q (n x nev, ldq) or null.
 cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q, int64_t ldq,
-                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st) {
+                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st, int64_t k0v, int64_t k1v,
+                     int64_t* vlo_out) {
   cudaError_t e;
   *nfail_out = 0;
   if (nev <= 0) return cudaSuccess;
@@ -385,6 +388,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     cudaMemcpyAsync(d_m, tm.data(), sizeof(int64_t) * ntask, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_i, ti.data(), sizeof(int64_t) * ntask, cudaMemcpyHostToDevice, st);
     // per-block g: launch per distinct block bound only when split (rare); common case one block
+    KScope ks(KC_TRID_BISECT, st, (int)(nblk == 1 ? 1 : nblk));
     if (nblk == 1) {
       td_bisect_kernel<<<(unsigned)((ntask + 127) / 128), 128, 0, st>>>(w.a2, d_s0, d_m, d_i, ntask, gb[0], pivmin,
                                                                         w.lamc);
@@ -437,33 +441,40 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
   cudaMemcpyAsync(w.gblk, gv.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(w.vblk, vb.data(), sizeof(int64_t) * 2 * nev, cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(w.nfail, 0, sizeof(int), st);
-  for (int64_t c0 = 0; c0 < nev; c0 += w.batch) {
-    int64_t nb = std::min(w.batch, nev - c0);
+  // vectors [vlo, vhi): the requested range [k0v, k1v) plus the reorthogonalisation window and
+  // the cluster members before it (ghost vectors, discarded by the caller)
+  const int W = prm.reorth_w;
+  const int64_t vhi = k1v;
+  int64_t vlo = std::min<int64_t>(std::max<int64_t>(0, k0v - W), clus_start[k0v]);
+  if (vlo_out) *vlo_out = vlo;
+  for (int64_t c0 = vlo; c0 < vhi; c0 += w.batch) {
+    int64_t nb = std::min(w.batch, vhi - c0);
     InvArgs a;
     a.alpha = alpha_d; a.vs0 = w.vblk; a.vm = w.vblk + nev; a.lam = w.lamv; a.gblk = w.gblk;
-    a.nvec = nb; a.col0 = c0; a.Q = Q; a.ldq = ldq; a.n = n;
+    a.nvec = nb; a.col0 = c0; a.qoff = vlo; a.Q = Q; a.ldq = ldq; a.n = n;
     size_t stride = (size_t)n * nb;
     a.wa = w.inv; a.wb = w.inv + stride; a.wc = w.inv + 2 * stride; a.wd = w.inv + 3 * stride; a.y = w.inv + 4 * stride;
     a.win = w.inv_in; a.seed = prm.seed; a.nfail = w.nfail;
+    KScope ks(KC_TRID_INV, st);
     td_inverse_kernel<<<(unsigned)((nb + 63) / 64), 64, 0, st>>>(a);
   }
   e = cudaGetLastError();
   if (e) return e;
   // re-orthogonalisation in blocks of 32 (descending order)
-  const int W = prm.reorth_w;
-  for (int64_t k0 = 0; k0 < nev; k0 += kReorthNB) {
-    int nb = (int)std::min<int64_t>(kReorthNB, nev - k0);
-    int64_t p0 = std::max<int64_t>(0, k0 - W);
-    int64_t cs = clus_start[k0];
+  for (int64_t k0 = vlo; k0 < vhi; k0 += kReorthNB) {
+    int nb = (int)std::min<int64_t>(kReorthNB, vhi - k0);
+    int64_t p0 = std::max<int64_t>(vlo, k0 - W);
+    int64_t cs = std::max<int64_t>(vlo, clus_start[k0]);
     if (cs < p0) p0 = cs;
-    double* Y = Q + SK_IDX(0, k0, ldq);
+    double* Y = Q + SK_IDX(0, k0 - vlo, ldq);
     // CGS2 against [p0, k0) in chunks of <= 64 previous vectors
     for (int pass = 0; pass < 2; pass++) {
       for (int64_t q0 = p0; q0 < k0; q0 += 64) {
         int p = (int)std::min<int64_t>(64, k0 - q0);
-        const double* Qp = Q + SK_IDX(0, q0, ldq);
+        const double* Qp = Q + SK_IDX(0, q0 - vlo, ldq);
         e = reorth_project(Qp, ldq, p, Y, ldq, nb, n, w, st);
         if (e) return e;
+        KScope ks(KC_TRID_REORTH, st);
         td_sub_proj<<<(unsigned)((n + 127) / 128), 128, (size_t)p * nb * 8, st>>>(Qp, ldq, p, w.H, Y, ldq, nb, n);
       }
     }
@@ -472,6 +483,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
       for (int pass = 0; pass < 2; pass++) {
         e = reorth_project(Y, ldq, nb, Y, ldq, nb, n, w, st);
         if (e) return e;
+        KScope ks(KC_TRID_REORTH, st, 2);
         td_chol_inv<<<1, 128, 0, st>>>(w.H, nb, w.Rinv);
         td_apply_rinv<<<(unsigned)((n + 127) / 128), 128, (size_t)nb * nb * 8, st>>>(Y, ldq, nb, w.Rinv, n);
       }
@@ -488,6 +500,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
 cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st) {
   if (nev <= 0) return cudaSuccess;
   dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)nev);
+  KScope ks(KC_ASSEMBLE, st);
   assemble_D_kernel<<<grid, 256, 0, st>>>(Q, ldq, n, nev, X, ldx);
   return cudaGetLastError();
 }

@@ -27,3 +27,29 @@ from .gen import (splitmix64, uniform_pm1, random_skew, random_skew_lower_colmaj
 
 __all__ = ["splitmix64", "uniform_pm1", "random_skew", "random_skew_lower_colmajor",
            "skew_toeplitz", "planted_skew", "bse_spd", "J_matrix"]
+
+
+def build_device_lib(force=False):
+    """Compile skewgen.cu -> libskewgen.so (input generation only)."""
+    import os
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    src = os.path.join(here, "skewgen.cu")
+    lib = os.path.join(here, "libskewgen.so")
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-Xcompiler", "-fPIC", "-shared", "-o", lib + ".tmp", src])
+        os.replace(lib + ".tmp", lib)
+    return lib
+
+
+def random_skew_lower_device(A, n, seed, stream=0):
+    """Fill the column-major CUDA buffer A (ld = A.stride(1)) with the strictly-lower
+    random skew matrix of (n, seed) -- bit-identical to random_skew(n, seed)."""
+    import ctypes
+    L = ctypes.CDLL(build_device_lib())
+    f = L.skewgen_random_skew_lower_device
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p]
+    rc = f(ctypes.c_void_p(A.data_ptr()), n, A.stride(1), seed, ctypes.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError(f"skewgen device kernel failed: {rc}")
