@@ -183,120 +183,192 @@ __global__ void band_copy_kernel(const double* ABin, int64_t ldin, int64_t n, in
 }
 
 // ------------------------------------------------------------------------------------
-// BT2 group compact-WY T (forward dlarft) from the staircase V_g: column c has its b
-// entries at local rows c .. c+b-1.  Gram G[c][c'] (c < c') = sum_d v_c[c'-c+d] v_c'[d].
-__global__ void bt2_tbuild_kernel(const double* qv, const double* qtau, int64_t ngroups, int k2, int b, double* qT) {
-  extern __shared__ double sh[];
-  double* G = sh;                 // k2 x k2
-  double* V = sh + k2 * k2;       // k2 x b
+// BT2 group prep: for group g (reflectors of sweeps s0..s0+K2-1 at chase position t) build
+// the dense staircase V (window rows rho = 0..RW-1 start at row s0 + t*b, reflector c at rows
+// rho = c+1 .. c+b), its forward compact-WY T (Q_g = I - V T V^T, dlarft from the Gram
+// matrix) and U = V T^T, stored as Ud[g][c][rho] (so that Q_g X = X - V (U^T X)).
+template <int K2, int RW>
+__global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const double* qtau, int64_t ngroups, int b,
+                                                      double* Ud) {
+  __shared__ double V[K2][RW];
+  __shared__ double G[K2][K2 + 1];
+  __shared__ double T[K2][K2 + 1];
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    const double* v = qv + g * k2 * b;
-    for (int e = threadIdx.x; e < k2 * b; e += blockDim.x) V[e] = v[e];
+    for (int e = threadIdx.x; e < K2 * RW; e += blockDim.x) (&V[0][0])[e] = 0.0;
     __syncthreads();
-    for (int e = threadIdx.x; e < k2 * k2; e += blockDim.x) {
-      int c = e % k2, c2 = e / k2;
-      double s = 0.0;
-      if (c < c2) {
-        int off = c2 - c;
-        for (int d = 0; d + off < b; d++) s += V[c * b + off + d] * V[c2 * b + d];
-      }
-      G[c + c2 * k2] = s;
+    const double* v = qv + g * K2 * b;
+    for (int e = threadIdx.x; e < K2 * b; e += blockDim.x) {
+      int c = e / b, d = e % b;
+      V[c][c + 1 + d] = v[e];
     }
     __syncthreads();
-    const double* tau = qtau + g * k2;
-    double* T = qT + g * k2 * k2;
-    for (int r = threadIdx.x; r < k2; r += blockDim.x) {
-      double trow[64];
-      for (int c = 0; c < k2; c++) trow[c] = 0.0;
-      trow[r] = tau[r];
-      for (int c = r + 1; c < k2; c++) {
+    for (int e = threadIdx.x; e < K2 * K2; e += blockDim.x) {
+      int c = e % K2, c2 = e / K2;
+      double s = 0.0;
+      if (c < c2)
+        for (int r = c2 + 1; r <= c + b && r < RW; r++) s += V[c][r] * V[c2][r];
+      G[c][c2] = s;
+    }
+    __syncthreads();
+    const double* tau = qtau + g * K2;
+    for (int r = threadIdx.x; r < K2; r += blockDim.x) {
+      for (int c = 0; c < K2; c++) T[r][c] = 0.0;
+      T[r][r] = tau[r];
+      for (int c = r + 1; c < K2; c++) {
         double s = 0.0;
-        for (int l = r; l < c; l++) s += trow[l] * G[l + c * k2];
-        trow[c] = -tau[c] * s;
+        for (int l = r; l < c; l++) s += T[r][l] * G[l][c];
+        T[r][c] = -tau[c] * s;
       }
-      for (int c = 0; c < k2; c++) T[r + c * k2] = trow[c];
+    }
+    __syncthreads();
+    double* U = Ud + g * K2 * RW;
+    for (int e = threadIdx.x; e < K2 * RW; e += blockDim.x) {
+      int c = e / RW, rho = e % RW;
+      double s = 0.0;
+      for (int c2 = c; c2 < K2; c2++) s += V[c2][rho] * T[c][c2];
+      U[e] = s;
     }
     __syncthreads();
   }
 }
 
-// BT2 apply: one CTA per column strip of X (NB columns); groups in order
-// (sweep blocks last -> first, t ascending).  Per group:  Z = V^T Xw (DMMA),
-// Z2 = T Z, Xw -= V Z2 (DMMA), Xw = X[R0 : R0+b+k2-1, strip].
-template <int NB, int K2, int MAXROWS>
-__global__ void __launch_bounds__(256) bt2_apply_kernel(double* X, int64_t ldx, int64_t ncols, int64_t n, int b,
-                                                       const double* qv, const double* qT, const int64_t* gofs,
-                                                       int64_t nblk) {
-  constexpr int LDV = MAXROWS + 4;     // Vs[c][rho]
-  constexpr int LDX = MAXROWS + 4;     // Xs[col][rho]
-  constexpr int LDZ = K2 + 4;          // Zs[col][c]
-  static_assert(LDV % 16 == 4 && LDZ % 16 == 4, "pad");
+// BT2 apply: one CTA per strip of NB columns of X, persistent over all groups in the
+// order sweep blocks last -> first, t ascending.  The RW-row window
+// X[W0 : W0+RW, strip] (W0 = s0 + t*b) lives in a RING-row shared-memory ring: step t+1
+// reuses the last RW-b rows of window t, so per step only b new rows are loaded (cp.async,
+// prefetched during step t) and b rows are written back.  The next group's V (packed
+// staircase) and U are prefetched into a second buffer.  Per step:
+//   Z = U^T Xw   (K2 x NB, DMMA, skip U's zero upper triangle)
+//   Xw -= V Z    (RW x NB, DMMA, skip the staircase's zero fragments)
+template <int NB, int K2, int RW, int RING, int BB>
+struct BT2Cfg {
+  static constexpr int LDX = RING + 4;   // Xs[col][slot]
+  static constexpr int LDU = RW + 4;     // Us[c][rho]
+  static constexpr int LDV = BB + 4;     // Vs[c][d]  (packed staircase, d = rho - c - 1)
+  static constexpr int LDZ = K2 + 4;     // Zs[col][c]
+  static constexpr int XS = NB * LDX, US = K2 * LDU, VS = K2 * LDV, ZS = NB * LDZ;
+  static constexpr size_t SMEM = (size_t)(XS + 2 * US + 2 * VS + ZS) * sizeof(double);
+  static_assert(LDX % 16 == 4 && LDU % 16 == 4 && LDZ % 16 == 4, "pad");
+  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB, "ring");
+};
+
+template <int NB, int K2, int RW, int RING, int BB>
+__global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols,
+                                                          int64_t n, const double* __restrict__ qv,
+                                                          const double* __restrict__ Ud,
+                                                          const int64_t* __restrict__ gofs, int64_t nblk) {
+  using C = BT2Cfg<NB, K2, RW, RING, BB>;
   extern __shared__ __align__(16) double sh[];
-  double* Vs = sh;                         // K2 * LDV
-  double* Ts = Vs + K2 * LDV;              // K2 * K2
-  double* Xs = Ts + K2 * K2;               // NB * LDX
-  double* Zs = Xs + NB * LDX;              // NB * LDZ
-  double* Z2 = Zs + NB * LDZ;              // NB * LDZ
+  double* Xs = sh;
+  double* Us0 = Xs + C::XS;
+  double* Vs0 = Us0 + 2 * C::US;
+  double* Zs = Vs0 + 2 * C::VS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
   const int64_t col0 = (int64_t)blockIdx.x * NB;
   const int ncl = (int)smin<int64_t>(NB, ncols - col0);
+  const bool vec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+
+  // async loads -------------------------------------------------------------------
+  auto load_group = [&](int64_t g, int buf) {   // U (K2 x RW) and packed V (K2 x BB)
+    double* Us = Us0 + buf * C::US;
+    double* Vs = Vs0 + buf * C::VS;
+    const double* u = Ud + g * K2 * RW;
+    const double* v = qv + g * K2 * BB;
+    for (int e = tid; e < K2 * RW / 2; e += 256) {
+      int c = e / (RW / 2), r = (e % (RW / 2)) * 2;
+      cp_async16(Us + c * C::LDU + r, u + c * RW + r, 16);
+    }
+    for (int e = tid; e < K2 * BB / 2; e += 256) {
+      int c = e / (BB / 2), d = (e % (BB / 2)) * 2;
+      cp_async16(Vs + c * C::LDV + d, v + c * BB + d, 16);
+    }
+  };
+  auto load_rows = [&](int64_t r0, int nrows, int slot0) {   // rows [r0, r0+nrows) -> ring slots slot0..
+    for (int e = tid; e < NB * nrows / 2; e += 256) {
+      int cl = e / (nrows / 2), rr = (e % (nrows / 2)) * 2;
+      int slot = slot0 + rr;
+      if (slot >= RING) slot -= RING;
+      int64_t r = r0 + rr;
+      double* dst = Xs + cl * C::LDX + slot;
+      const double* src = X + SK_IDX(r, col0 + cl, ldx);
+      int cnt = (cl < ncl) ? (int)smin<int64_t>(2, smax<int64_t>(0, n - r)) : 0;
+      if (vec) {
+        cp_async16(dst, cnt ? src : X, cnt * 8);
+      } else {
+        cp_async8(dst, cnt > 0 ? src : X, cnt > 0 ? 8 : 0);
+        cp_async8(dst + 1, cnt > 1 ? src + 1 : X, cnt > 1 ? 8 : 0);
+      }
+    }
+  };
+  auto store_rows = [&](int64_t r0, int nrows, int slot0) {
+    for (int e = tid; e < NB * nrows; e += 256) {
+      int cl = e / nrows, rr = e % nrows;
+      int slot = slot0 + rr;
+      if (slot >= RING) slot -= RING;
+      int64_t r = r0 + rr;
+      if (cl < ncl && r < n) X[SK_IDX(r, col0 + cl, ldx)] = Xs[cl * C::LDX + slot];
+    }
+  };
+
+  int buf = 0;
+  if (nblk <= 0) return;
+  {
+    const int64_t blk = nblk - 1;
+    load_group(gofs[blk], 0);
+    load_rows(blk * K2, RW, 0);
+    cp_async_commit();
+  }
   for (int64_t blk = nblk - 1; blk >= 0; blk--) {
     const int64_t s0 = blk * K2;
-    const int64_t ntask = 1 + (n - 3 - s0) / b;
+    const int64_t ntask = 1 + (n - 3 - s0) / BB;
     for (int64_t t = 0; t < ntask; t++) {
-      const int64_t g = gofs[blk] + t;
-      const int64_t R0 = s0 + 1 + t * b;
-      const int rows = (int)smin<int64_t>(b + K2 - 1, n - R0);
-      // load V (staircase), T, X window
-      for (int e = tid; e < K2 * MAXROWS; e += 256) {
-        int c = e / MAXROWS, rho = e % MAXROWS;
-        int d = rho - c;
-        Vs[c * LDV + rho] = (d >= 0 && d < b && rho < rows) ? qv[(g * K2 + c) * b + d] : 0.0;
-      }
-      for (int e = tid; e < K2 * K2; e += 256) Ts[e] = qT[g * K2 * K2 + e];
-      for (int e = tid; e < NB * MAXROWS; e += 256) {
-        int cl = e / MAXROWS, rho = e % MAXROWS;
-        Xs[cl * LDX + rho] = (cl < ncl && rho < rows) ? X[SK_IDX(R0 + rho, col0 + cl, ldx)] : 0.0;
-      }
+      const int64_t W0 = s0 + t * BB;
+      const int off = (int)((t * BB) % RING);
+      cp_async_wait<0>();
       __syncthreads();
-      // Z = V^T Xw : M = K2, N = NB, K = MAXROWS.  warps: (K2/8) x (8/(K2/8)) grid
+      // ---- prefetch the next group (and the next rows of the window, same block)
+      if (t + 1 < ntask) {
+        load_group(gofs[blk] + t + 1, buf ^ 1);
+        int so = off + RW;
+        if (so >= RING) so -= RING;
+        load_rows(W0 + RW, BB, so);
+      } else if (blk > 0) {
+        load_group(gofs[blk - 1], buf ^ 1);
+      }
+      cp_async_commit();
+      const double* Us = Us0 + buf * C::US;
+      const double* Vs = Vs0 + buf * C::VS;
+      // ---- Z = U^T Xw : M = K2 (c), N = NB (col), K = RW (rho); warps 4 (M) x 2 (N)
       {
-        constexpr int WMR = K2 / 8;                 // warps along M (8-row tiles)
-        constexpr int WNR = 8 / WMR;                // warps along N
-        constexpr int FN = NB / (8 * WNR);
-        const int wm = warp % WMR, wn = warp / WMR;
+        constexpr int FN = NB / 16;
+        const int m0 = (warp & 3) * 8, n0 = (warp >> 2) * (NB / 2);
         double acc[FN][2];
 #pragma unroll
         for (int j = 0; j < FN; j++) acc[j][0] = acc[j][1] = 0.0;
-        for (int kk = 0; kk < MAXROWS; kk += 4) {
-          double af = Vs[(wm * 8 + gq) * LDV + kk + tq];
+        // U[rho][c] = 0 for rho <= c: k blocks with kk + 3 <= m0 are zero
+#pragma unroll 4
+        for (int kk = (m0 / 4) * 4; kk < RW; kk += 4) {
+          double af = Us[(m0 + gq) * C::LDU + kk + tq];
+          int slot = off + kk;
+          if (slot >= RING) slot -= RING;
 #pragma unroll
           for (int j = 0; j < FN; j++) {
-            double bf = Xs[(wn * FN * 8 + j * 8 + gq) * LDX + kk + tq];
+            double bf = Xs[(n0 + 8 * j + gq) * C::LDX + slot + tq];
             dmma884(acc[j][0], acc[j][1], af, bf);
           }
         }
 #pragma unroll
         for (int j = 0; j < FN; j++) {
-          int m = wm * 8 + gq, nn = wn * FN * 8 + j * 8 + 2 * tq;
-          Zs[nn * LDZ + m] = acc[j][0];
-          Zs[(nn + 1) * LDZ + m] = acc[j][1];
+          int nn = n0 + 8 * j + 2 * tq;
+          Zs[nn * C::LDZ + m0 + gq] = acc[j][0];
+          Zs[(nn + 1) * C::LDZ + m0 + gq] = acc[j][1];
         }
       }
       __syncthreads();
-      // Z2 = T Z  (T upper triangular)
-      for (int e = tid; e < K2 * NB; e += 256) {
-        int c = e % K2, cl = e / K2;
-        double s = 0.0;
-        for (int l = c; l < K2; l++) s += Ts[c + l * K2] * Zs[cl * LDZ + l];
-        Z2[cl * LDZ + c] = s;
-      }
-      __syncthreads();
-      // Xw -= V Z2 : M = MAXROWS, N = NB, K = K2; warps 4 (M) x 2 (N)
+      // ---- Xw -= V Z : M = RW (rho), N = NB, K = K2 (c); warps 4 (M, RW/4 rows) x 2 (N)
       {
-        constexpr int FM = MAXROWS / 32;    // 8-row fragments per warp along M (4 warps)
-        constexpr int FN = NB / 16;         // 2 warps along N
-        const int wm = warp % 4, wn = warp / 4;
+        constexpr int FM = RW / 32, FN = NB / 16;
+        const int wm = warp & 3, n0 = (warp >> 2) * (NB / 2);
         double acc[FM][FN][2];
 #pragma unroll
         for (int i = 0; i < FM; i++)
@@ -304,33 +376,48 @@ __global__ void __launch_bounds__(256) bt2_apply_kernel(double* X, int64_t ldx, 
           for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < K2; kk += 4) {
-          double af[FM], bf[FN];
+          double bf[FN];
 #pragma unroll
-          for (int i = 0; i < FM; i++) af[i] = Vs[(kk + tq) * LDV + wm * FM * 8 + i * 8 + gq];
+          for (int j = 0; j < FN; j++) bf[j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
 #pragma unroll
-          for (int j = 0; j < FN; j++) bf[j] = Z2[(wn * FN * 8 + j * 8 + gq) * LDZ + kk + tq];
+          for (int i = 0; i < FM; i++) {
+            const int m0 = wm * (RW / 4) + 8 * i;
+            // staircase: V[rho][c] != 0 iff 1 <= rho - c <= BB
+            if (m0 + 7 - kk < 1 || m0 - (kk + 3) > BB) continue;
+            const int rho = m0 + gq, c = kk + tq;
+            const int d = rho - c - 1;
+            double af = (d >= 0 && d < BB) ? Vs[c * C::LDV + d] : 0.0;
 #pragma unroll
-          for (int i = 0; i < FM; i++)
-#pragma unroll
-            for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], af, bf[j]);
+          }
         }
 #pragma unroll
-        for (int i = 0; i < FM; i++)
+        for (int i = 0; i < FM; i++) {
+          const int m0 = wm * (RW / 4) + 8 * i;
+          int slot = off + m0;
+          if (slot >= RING) slot -= RING;
 #pragma unroll
           for (int j = 0; j < FN; j++) {
-            int m = wm * FM * 8 + i * 8 + gq, nn = wn * FN * 8 + j * 8 + 2 * tq;
-            Xs[nn * LDX + m] -= acc[i][j][0];
-            Xs[(nn + 1) * LDX + m] -= acc[i][j][1];
+            int nn = n0 + 8 * j + 2 * tq;
+            Xs[nn * C::LDX + slot + gq] -= acc[i][j][0];
+            Xs[(nn + 1) * C::LDX + slot + gq] -= acc[i][j][1];
           }
+        }
       }
       __syncthreads();
-      for (int e = tid; e < NB * MAXROWS; e += 256) {
-        int cl = e / MAXROWS, rho = e % MAXROWS;
-        if (cl < ncl && rho < rows) X[SK_IDX(R0 + rho, col0 + cl, ldx)] = Xs[cl * LDX + rho];
+      // ---- write back the rows leaving the window
+      if (t + 1 < ntask) {
+        store_rows(W0, BB, off);
+      } else {
+        store_rows(W0, RW, off);
+        __syncthreads();
+        if (blk > 0) load_rows((blk - 1) * K2, RW, 0);   // first window of the next block
+        cp_async_commit();
       }
-      __syncthreads();
+      buf ^= 1;
     }
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------------------
@@ -366,7 +453,7 @@ void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w) {
   int64_t ng = std::max<int64_t>(L.ngroups, 1);
   w.qv = ar.take<double>((size_t)ng * L.k2 * L.b);
   w.qtau = ar.take<double>((size_t)ng * L.k2);
-  if (vectors) w.qT = ar.take<double>((size_t)ng * L.k2 * L.k2);
+  if (vectors) w.qT = ar.take<double>((size_t)ng * L.k2 * (L.b + L.k2));   // U_g (k2 x (b+k2)) per group
   w.gofs = ar.take<int64_t>(std::max<int64_t>(L.nblk, 1));
 }
 
@@ -411,24 +498,20 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
 cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st) {
   if (L.n <= 2 || L.ngroups == 0 || ncols == 0) return cudaSuccess;
   cudaError_t e;
-  const int k2 = L.k2, b = L.b;
+  constexpr int NB = 64, K2 = 32, RW = 96, RING = 192, BB = 64;
+  if (L.k2 != K2 || L.b != BB) return cudaErrorInvalidValue;
   {
-  KScope ks(KC_BT2_T, st);
-  bt2_tbuild_kernel<<<(unsigned)std::min<int64_t>(L.ngroups, 4096), 128, (size_t)(k2 * k2 + k2 * b) * 8, st>>>(
-      w.qv, w.qtau, L.ngroups, k2, b, w.qT);
+    KScope ks(KC_BT2_T, st);
+    bt2_prep_kernel<K2, RW><<<(unsigned)std::min<int64_t>(L.ngroups, 8 * 148), 128, 0, st>>>(w.qv, w.qtau, L.ngroups,
+                                                                                              BB, w.qT);
   }
-  constexpr int NB = 64, K2 = 32, MAXROWS = 96;
-  if (k2 != K2 || b + k2 - 1 > MAXROWS) return cudaErrorInvalidValue;
-  size_t smem = (size_t)(K2 * (MAXROWS + 4) + K2 * K2 + NB * (MAXROWS + 4) + 2 * NB * (K2 + 4)) * 8;
-  static bool set = false;
-  if (!set) {
-    e = cudaFuncSetAttribute(bt2_apply_kernel<NB, K2, MAXROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    set = true;
-  }
+  using Cf = BT2Cfg<NB, K2, RW, RING, BB>;
+  e = cudaFuncSetAttribute(bt2_apply_kernel<NB, K2, RW, RING, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)Cf::SMEM);
+  if (e) return e;
   KScope ks(KC_BT2, st);
-  bt2_apply_kernel<NB, K2, MAXROWS><<<(unsigned)((ncols + NB - 1) / NB), 256, smem, st>>>(X, ldx, ncols, L.n, b, w.qv,
-                                                                                         w.qT, w.gofs, L.nblk);
+  bt2_apply_kernel<NB, K2, RW, RING, BB><<<(unsigned)((ncols + NB - 1) / NB), 256, Cf::SMEM, st>>>(
+      X, ldx, ncols, L.n, w.qv, w.qT, w.gofs, L.nblk);
   return cudaGetLastError();
 }
 

@@ -58,22 +58,27 @@ __global__ void td_bisect_kernel(const double* a2, const int64_t* task_s0, const
   out[q] = 0.5 * (lo + hi);
 }
 
-// Inverse iteration, one thread per vector.  Work arrays interleaved [row][batch].
+// Inverse iteration, one thread per vector (dstein semantics).  Work arrays
+// are interleaved [row][batch] so that a warp's accesses are coalesced; every pass over a
+// vector is chunked by IU rows with the chunk's loads issued first (they never depend on
+// the loop-carried values), so each thread keeps IU loads in flight.  The scaling of the
+// right-hand side is folded into the forward pass and the 1-norm / max-norm / 2-norm of
+// the solution are accumulated in the back substitution.
 struct InvArgs {
   const double* alpha;          // global alpha (n-1)
-  const int64_t* vs0; const int64_t* vm;   // block start / size per vector
+  const int64_t* vs0; const int64_t* vm;   // block start / size per vector (global index)
   const double* lam;            // perturbed eigenvalue per vector
   const double* gblk;           // block Gershgorin bound per vector
   int64_t nvec; int64_t col0;   // vectors [col0, col0+nvec) (global eigenpair indices)
-  int64_t qoff;                 // Q column of global index g is g - qoff
-  double* Q; int64_t ldq; int64_t n;
-  double *wa, *wb, *wc, *wd; unsigned char* win;   // [mmax][nvec]
-  double* y;                    // [mmax][nvec]
+  double *wa, *wb, *wc, *wd; unsigned char* win;   // [m][nvec]
+  double* y;                    // [m][nvec]
+  double* scale;                // [nvec] final 1/||y|| with the dstein sign
   uint64_t seed;
   int* nfail;
 };
 
-__global__ void td_inverse_kernel(InvArgs a) {
+template <int IU>
+__global__ void __launch_bounds__(128) td_inverse_kernel(InvArgs a) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= a.nvec) return;
   const int64_t gv = a.col0 + q;
@@ -85,89 +90,128 @@ __global__ void td_inverse_kernel(InvArgs a) {
   const double lambda = a.lam[gv];
   const double g = a.gblk[gv];
   const double eps = DBL_EPSILON;
-  if (m == 1) {
-    for (int64_t i = 0; i < a.n; i++) a.Q[SK_IDX(i, gv - a.qoff, a.ldq)] = (i == s0) ? 1.0 : 0.0;
-    return;
-  }
-  // dlagtf: LU of T - lambda I with partial pivoting
-  for (int64_t k = 0; k < m; k++) { AT(A_, k) = -lambda; AT(IN, k) = 0; }
-  for (int64_t k = 0; k + 1 < m; k++) { double e = a.alpha[s0 + k]; AT(Bb, k) = e; AT(C, k) = e; }
-  for (int64_t k = 0; k + 1 < m; k++) {
-    double ak = AT(A_, k), bk = AT(Bb, k), ck = AT(C, k), ak1 = AT(A_, k + 1);
-    double bk1 = (k + 2 < m) ? AT(Bb, k + 1) : 0.0;
-    double scale1 = fabs(ak) + fabs(bk);
-    double scale2 = fabs(ck) + fabs(ak1) + fabs(bk1);
-    double piv1 = (scale1 == 0.0) ? 0.0 : fabs(ak) / scale1;
-    if (ck == 0.0) {
-      AT(IN, k) = 0;
-      if (k + 2 < m) AT(D, k) = 0.0;
-    } else {
-      double piv2 = fabs(ck) / scale2;
-      if (piv2 <= piv1) {
-        AT(IN, k) = 0;
-        double cm = ck / ak;
-        AT(C, k) = cm;
-        AT(A_, k + 1) = ak1 - cm * bk;
-        if (k + 2 < m) AT(D, k) = 0.0;
-      } else {
-        AT(IN, k) = 1;
-        double mult = ak / ck;
-        AT(A_, k) = ck;
-        AT(A_, k + 1) = bk - mult * ak1;
-        if (k + 2 < m) { AT(D, k) = bk1; AT(Bb, k + 1) = -mult * bk1; }
-        AT(Bb, k) = ak1;
-        AT(C, k) = mult;
-      }
-    }
-  }
+  if (m == 1) { AT(y, 0) = 1.0; a.scale[q] = 1.0; return; }
+  const double* al = a.alpha + s0;
+  // ---- dlagtf: LU of T - lambda I with partial pivoting; tol = eps * max|U entries|
   double tol = 0.0;
-  for (int64_t k = 0; k < m; k++) {
-    tol = fmax(tol, fabs(AT(A_, k)));
-    if (k + 1 < m) tol = fmax(tol, fabs(AT(Bb, k)));
-    if (k + 2 < m) tol = fmax(tol, fabs(AT(D, k)));
+  {
+    double ak = -lambda, bk = al[0];     // current (k) diagonal and super-diagonal
+    for (int64_t k = 0; k + 1 < m; k++) {
+      const double ck = al[k];
+      const double ak1 = -lambda;
+      const double bk1 = (k + 2 < m) ? al[k + 1] : 0.0;
+      const double scale1 = fabs(ak) + fabs(bk);
+      const double scale2 = fabs(ck) + fabs(ak1) + fabs(bk1);
+      const double piv1 = (scale1 == 0.0) ? 0.0 : fabs(ak) / scale1;
+      double na1, nb1 = bk1, dk = 0.0, cout;
+      unsigned char in = 0;
+      if (ck == 0.0) {
+        cout = ck; na1 = ak1;
+      } else {
+        const double piv2 = fabs(ck) / scale2;
+        if (piv2 <= piv1) {
+          cout = ck / ak;
+          na1 = ak1 - cout * bk;
+        } else {
+          in = 1;
+          const double mult = ak / ck;
+          const double ak_new = ck;
+          na1 = bk - mult * ak1;
+          dk = bk1;
+          nb1 = -mult * bk1;
+          const double bk_new = ak1;
+          ak = ak_new; bk = bk_new; cout = mult;
+        }
+      }
+      AT(A_, k) = ak; AT(Bb, k) = bk; AT(C, k) = cout; AT(IN, k) = in;
+      if (k + 2 < m) AT(D, k) = dk;
+      tol = fmax(tol, fmax(fabs(ak), fabs(bk)));
+      if (k + 2 < m) tol = fmax(tol, fabs(dk));
+      ak = na1; bk = nb1;
+    }
+    AT(A_, m - 1) = ak;
+    tol = fmax(tol, fabs(ak));
   }
   tol *= eps;
   if (tol == 0.0) tol = eps;
-  // start vector
+  const double anm1 = fabs(AT(A_, m - 1));
+  // ---- start vector (uniform [-1, 1) from the counter-based generator)
+  double asum = 0.0;
   for (int64_t i = 0; i < m; i++) {
     uint64_t z = td_splitmix64(a.seed * 0x9E3779B97F4A7C15ull + (uint64_t)gv * 0x100000001B3ull + (uint64_t)i);
-    AT(y, i) = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+    double v = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+    AT(y, i) = v;
+    asum += fabs(v);
   }
   const double dtpcrt = sqrt(0.1 / (double)m);
   const double sfmin = DBL_MIN, bignum = 1.0 / DBL_MIN;
   int nrmchk = 0, ok = 0;
+  double ssq = 0.0, ymax = 0.0;
+  int64_t jmax = 0;
   for (int its = 0; its < 5; its++) {
-    double asum = 0.0;
-    for (int64_t i = 0; i < m; i++) asum += fabs(AT(y, i));
-    double scl = (double)m * g * fmax(eps, fabs(AT(A_, m - 1))) / asum;
-    for (int64_t i = 0; i < m; i++) AT(y, i) *= scl;
-    // dlagts(-1): forward
-    for (int64_t k = 1; k < m; k++) {
-      if (AT(IN, k - 1) == 0) AT(y, k) -= AT(C, k - 1) * AT(y, k - 1);
-      else { double tmp = AT(y, k - 1); AT(y, k - 1) = AT(y, k); AT(y, k) = tmp - AT(C, k - 1) * AT(y, k); }
-    }
-    // back with perturbation
-    double nrm = 0.0;
-    for (int64_t k = m - 1; k >= 0; k--) {
-      double temp;
-      if (k + 2 < m) temp = AT(y, k) - AT(Bb, k) * AT(y, k + 1) - AT(D, k) * AT(y, k + 2);
-      else if (k + 1 < m) temp = AT(y, k) - AT(Bb, k) * AT(y, k + 1);
-      else temp = AT(y, k);
-      double ak = AT(A_, k);
-      double pert = copysign(tol, ak);
-      for (int guard = 0; guard < 2100; guard++) {
-        double absak = fabs(ak);
-        if (absak < 1.0) {
-          if (absak < sfmin) {
-            if (absak == 0.0 || fabs(temp) * sfmin > absak) { ak += pert; pert *= 2.0; continue; }
-            temp *= bignum; ak *= bignum;
-          } else if (fabs(temp) > absak * bignum) { ak += pert; pert *= 2.0; continue; }
-        }
-        break;
+    const double scl = (double)m * g * fmax(eps, anm1) / asum;
+    // ---- forward (dlagts job -1), scaling folded in: carry p = y[k-1]
+    double p = AT(y, 0) * scl;
+    for (int64_t k0 = 1; k0 < m; k0 += IU) {
+      double cc[IU], yy[IU];
+      unsigned char ii[IU];
+#pragma unroll
+      for (int u = 0; u < IU; u++) {
+        const int64_t k = k0 + u;
+        if (k < m) { cc[u] = AT(C, k - 1); ii[u] = AT(IN, k - 1); yy[u] = AT(y, k); }
       }
-      double yk = temp / ak;
-      AT(y, k) = yk;
-      nrm = fmax(nrm, fabs(yk));
+#pragma unroll
+      for (int u = 0; u < IU; u++) {
+        const int64_t k = k0 + u;
+        if (k < m) {
+          const double qv = yy[u] * scl;
+          if (ii[u] == 0) { AT(y, k - 1) = p; p = qv - cc[u] * p; }
+          else { AT(y, k - 1) = qv; p = p - cc[u] * qv; }
+        }
+      }
+    }
+    AT(y, m - 1) = p;
+    // ---- back substitution with perturbed pivots; carry y[k+1], y[k+2]
+    double y1 = 0.0, y2 = 0.0, nrm = 0.0;
+    asum = 0.0; ssq = 0.0; ymax = 0.0; jmax = 0;
+    for (int64_t k0 = m - 1; k0 >= 0; k0 -= IU) {
+      double aa[IU], bb[IU], dd[IU], yy[IU];
+#pragma unroll
+      for (int u = 0; u < IU; u++) {
+        const int64_t k = k0 - u;
+        if (k >= 0) {
+          aa[u] = AT(A_, k); yy[u] = AT(y, k);
+          bb[u] = (k + 1 < m) ? AT(Bb, k) : 0.0;
+          dd[u] = (k + 2 < m) ? AT(D, k) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < IU; u++) {
+        const int64_t k = k0 - u;
+        if (k >= 0) {
+          double temp = yy[u] - bb[u] * y1 - dd[u] * y2;
+          double ak = aa[u];
+          double pert = copysign(tol, ak);
+          for (int guard = 0; guard < 2100; guard++) {
+            double absak = fabs(ak);
+            if (absak < 1.0) {
+              if (absak < sfmin) {
+                if (absak == 0.0 || fabs(temp) * sfmin > absak) { ak += pert; pert *= 2.0; continue; }
+                temp *= bignum; ak *= bignum;
+              } else if (fabs(temp) > absak * bignum) { ak += pert; pert *= 2.0; continue; }
+            }
+            break;
+          }
+          const double yk = temp / ak;
+          AT(y, k) = yk;
+          y2 = y1; y1 = yk;
+          const double ay = fabs(yk);
+          asum += ay;
+          ssq += yk * yk;
+          if (ay > ymax || (ay == ymax && k < jmax)) { ymax = ay; jmax = k; }
+          nrm = fmax(nrm, ay);
+        }
+      }
     }
     if (nrm < dtpcrt) continue;
     nrmchk++;
@@ -176,21 +220,34 @@ __global__ void td_inverse_kernel(InvArgs a) {
     break;
   }
   if (!ok) atomicAdd(a.nfail, 1);
-  double s2 = 0.0;
-  int64_t jmax = 0;
-  double ymax = 0.0;
-  for (int64_t i = 0; i < m; i++) {
-    double v = AT(y, i);
-    s2 += v * v;
-    if (fabs(v) > ymax) { ymax = fabs(v); jmax = i; }
-  }
-  double scl = 1.0 / sqrt(s2);
-  if (AT(y, jmax) < 0) scl = -scl;
-  for (int64_t i = 0; i < a.n; i++) {
-    double v = (i >= s0 && i < s0 + m) ? AT(y, i - s0) * scl : 0.0;
-    a.Q[SK_IDX(i, gv - a.qoff, a.ldq)] = v;
-  }
+  double sc = 1.0 / sqrt(ssq);
+  if (AT(y, jmax) < 0) sc = -sc;
+  a.scale[q] = sc;
 #undef AT
+}
+
+// Q[:, qcol0 + q] = scale[q] * y[:, q] placed at the vector's block rows, zero elsewhere;
+// 32 x 32 tiles transposed through shared memory (coalesced on both sides).
+__global__ void td_place_vectors(const double* y, const double* scale, int64_t nvec, int64_t col0,
+                                 const int64_t* vs0, const int64_t* vm, int64_t n, double* Q, int64_t ldq,
+                                 int64_t qcol0) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, v0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int64_t row = r0 + rr, v = v0 + tx;
+    double val = 0.0;
+    if (v < nvec && row < n) {
+      const int64_t s0 = vs0[col0 + v], m = vm[col0 + v];
+      if (row >= s0 && row < s0 + m) val = y[(size_t)(row - s0) * nvec + v] * scale[v];
+    }
+    tile[rr][tx] = val;
+  }
+  __syncthreads();
+  for (int vv = ty; vv < 32; vv += 8) {
+    const int64_t v = v0 + vv, row = r0 + tx;
+    if (v < nvec && row < n) Q[SK_IDX(row, qcol0 + v, ldq)] = tile[tx][vv];
+  }
 }
 
 // ---------------- block re-orthogonalisation helpers
@@ -316,9 +373,9 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
   w.gblk = ar.take<double>(ne);
   w.vblk = ar.take<int64_t>(2 * ne);
   // bound the interleaved LU workspace to ~1 GiB
-  int64_t batch = std::max<int64_t>(1, std::min<int64_t>(ne, (int64_t)(1ll << 30) / (41 * nn)));
+  int64_t batch = std::max<int64_t>(1, std::min<int64_t>(ne, (int64_t)(16ll << 30) / (49 * nn)));
   w.batch = batch;
-  w.inv = ar.take<double>((size_t)5 * nn * batch);
+  w.inv = ar.take<double>((size_t)5 * nn * batch + batch);
   w.inv_in = ar.take<unsigned char>((size_t)nn * batch);
   w.nfail = ar.take<int>(1);
   int64_t nchunks = (nn + kGramRows - 1) / kGramRows;
@@ -451,12 +508,15 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     int64_t nb = std::min(w.batch, vhi - c0);
     InvArgs a;
     a.alpha = alpha_d; a.vs0 = w.vblk; a.vm = w.vblk + nev; a.lam = w.lamv; a.gblk = w.gblk;
-    a.nvec = nb; a.col0 = c0; a.qoff = vlo; a.Q = Q; a.ldq = ldq; a.n = n;
+    a.nvec = nb; a.col0 = c0;
     size_t stride = (size_t)n * nb;
     a.wa = w.inv; a.wb = w.inv + stride; a.wc = w.inv + 2 * stride; a.wd = w.inv + 3 * stride; a.y = w.inv + 4 * stride;
+    a.scale = w.inv + 5 * stride;
     a.win = w.inv_in; a.seed = prm.seed; a.nfail = w.nfail;
-    KScope ks(KC_TRID_INV, st);
-    td_inverse_kernel<<<(unsigned)((nb + 63) / 64), 64, 0, st>>>(a);
+    KScope ks(KC_TRID_INV, st, 2);
+    td_inverse_kernel<8><<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(a);
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((nb + 31) / 32));
+    td_place_vectors<<<grid, dim3(32, 8), 0, st>>>(a.y, a.scale, nb, c0, w.vblk, w.vblk + nev, n, Q, ldq, c0 - vlo);
   }
   e = cudaGetLastError();
   if (e) return e;
