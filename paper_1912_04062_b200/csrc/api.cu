@@ -260,7 +260,11 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   CK(trid_run(n, p.alpha, nev, p.lam, vec ? p.Q : nullptr, p.ldn, p.tw, c.prm, &nfail, st, k0, k1, &vlo),
      "tridiagonal");
   c.last_nfail = nfail;
-  if (vec) CK(assemble_D(p.Q + SK_IDX(0, k0 - vlo, p.ldn), p.ldn, n, nloc, p.X, p.ldn, st), "assemble D");
+  if (vec) {
+    CK(assemble_D(p.Q + SK_IDX(0, k0 - vlo, p.ldn), p.ldn, n, nloc, p.X, p.ldn, st), "assemble D");
+    if (p.ldn > n)   // zero padding row (read, unchanged, by the BT2 bulk copies when n is odd)
+      CK(cudaMemset2DAsync(p.X + n, p.ldn * 8, 0, (p.ldn - n) * 8, 2 * nloc, st), "pad row");
+  }
   tstop(ctx, ST_TRID);
   if (vec) {
     tstart(ctx, ST_BT2);

@@ -23,6 +23,8 @@
 #include <cooperative_groups.h>
 #include <vector>
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 
 namespace cg = cooperative_groups;
 
@@ -44,19 +46,20 @@ __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
   extern __shared__ __align__(16) double W[];     // window [2b cols][LDW]
   __shared__ double vs[MAXB], ws[MAXB], zs[MAXB], sc[4];
   const int b = a.b;
-  const int LDW = 2 * b + 2;
+  const int LDW = 2 * b + 2;   // LDW - 1 odd: the strided skew reads of D are conflict-free
   const int64_t n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t s = blockIdx.x; s < n - 2; s += gridDim.x) {
     const int64_t nt = chase_ntask(n, b, s);
     const int64_t ntprev = (s > 0) ? chase_ntask(n, b, s - 1) : 0;
     for (int64_t t = 0; t < nt; t++) {
-      // ---- wait for the previous sweep to be 4 tasks ahead (or finished)
+      // ---- sweep s task t may run once sweep s-1 finished tasks 0..t+2 (their entry sets
+      //      are then disjoint from this task's; checked against the sequential order)
       if (s > 0) {
         if (tid == 0) {
-          const int need = (int)smin<int64_t>(t + 4, ntprev);
+          const int need = (int)smin<int64_t>(t + 3, ntprev);
           volatile int* pr = a.progress + (s - 1);
-          while (*pr < need) { __nanosleep(64); }
+          while (*pr < need) { __nanosleep(32); }
           __threadfence();
         }
         __syncthreads();
@@ -66,20 +69,53 @@ __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
       else { col = s + 1 + (t - 1) * b; r = col + b; L = smin<int64_t>(b, n - r); }
       const int64_t e = smin<int64_t>(n, r + L + b);
       const int ncol = (int)(r + L - col);
-      // ---- load the touched entries: col c < r: rows [r, r+L); c >= r: rows [c, e)
-      for (int cc = warp; cc < ncol; cc += 8) {
-        int64_t c = col + cc;
-        int64_t lo = (c < r) ? r : c, hi = (c < r) ? r + L : e;
-        for (int64_t i = lo + lane; i < hi; i += 32) W[cc * LDW + (i - c)] = __ldcg(&a.AB[(i - c) + c * a.ldab]);
+      const int nl = (int)(r - col);          // columns of the left block (1 for t = 0)
+      const int ne = (int)(e - r - L);         // rows of the block below
+      const int dc = nl;                       // local column of r
+      // ---- load the touched entries: column cc (warp-strided) has rows [lo, hi) with
+      //      lo = r, hi = r+L for the left columns (c < r) and lo = c, hi = e otherwise.
+      //      Two columns x four rows per lane are loaded (L2-coherent __ldcg) before any
+      //      shared store, so eight loads are in flight per thread.
+      auto seg = [&](int cc, int64_t& lo, int64_t& hi) {
+        const int64_t c = col + cc;
+        lo = (c < r) ? r : c;
+        hi = (c < r) ? r + L : e;
+      };
+      for (int cc0 = warp; cc0 < ncol; cc0 += 16) {
+        double v[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int cc = cc0 + 8 * h;
+          int64_t lo = 0, hi = 0;
+          if (cc < ncol) seg(cc, lo, hi);
+          const int64_t c = col + cc;
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int64_t i = lo + lane + 32 * k;
+            v[h][k] = (cc < ncol && i < hi) ? __ldcg(&a.AB[(i - c) + c * a.ldab]) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int cc = cc0 + 8 * h;
+          if (cc >= ncol) continue;
+          int64_t lo, hi;
+          seg(cc, lo, hi);
+          const int64_t c = col + cc;
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int64_t i = lo + lane + 32 * k;
+            if (i < hi) W[cc * LDW + (int)(i - c)] = v[h][k];
+          }
+        }
       }
       __syncthreads();
       // ---- (a) Householder of x = A[r:r+L, col]  (dlarfg convention)
-      const int cx = 0;   // local column of col
       if (warp == 0) {
         double s2 = 0.0;
-        for (int i = 1 + lane; i < L; i += 32) { double x = W[cx * LDW + (r + i - col)]; s2 += x * x; }
+        for (int i = 1 + lane; i < L; i += 32) { double x = W[(r + i - col)]; s2 += x * x; }
         s2 = warp_sum(s2);
-        double x0 = W[cx * LDW + (r - col)];
+        double x0 = W[(r - col)];
         double beta, tau, scal;
         if (s2 == 0.0) { beta = x0; tau = 0.0; scal = 0.0; }
         else {
@@ -89,16 +125,15 @@ __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
           scal = 1.0 / (x0 - beta);
         }
         for (int i = lane; i < L; i += 32) {
-          double v = (i == 0) ? 1.0 : W[cx * LDW + (r + i - col)] * scal;
+          double v = (i == 0) ? 1.0 : W[(r + i - col)] * scal;
           vs[i] = v;
-          W[cx * LDW + (r + i - col)] = (i == 0) ? beta : 0.0;
+          W[(r + i - col)] = (i == 0) ? beta : 0.0;
         }
         if (lane == 0) sc[0] = tau;
       }
       __syncthreads();
       const double tau = sc[0];
-      // ---- store the reflector (v zero-padded to b by the initial memset)
-      {
+      {   // store the reflector (v zero-padded to b by the initial memset)
         const int64_t blk = s / a.k2, c = s % a.k2;
         const int64_t gidx = a.gofs[blk] + t;
         double* dst = a.qv + (gidx * a.k2 + c) * b;
@@ -106,46 +141,47 @@ __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
         if (tid == 0) a.qtau[gidx * a.k2 + c] = tau;
       }
       if (tau != 0.0) {
-        // ---- (b) left block: columns (col, r) (t >= 1): y = v^T A[r:r+L, c]; A -= tau v y
-        for (int cc = 1 + warp; cc < (int)(r - col); cc += 8) {
-          const int64_t c = col + cc;
+        // ---- (b) left block columns (col, r): y = tau v^T A[r:r+L, c]; A -= v y   (warp per column)
+        for (int cc = 1 + warp; cc < nl; cc += 8) {
+          const int d0 = nl - cc;   // row r sits at offset r - c = nl - cc
           double y = 0.0;
-          for (int i = lane; i < L; i += 32) y += vs[i] * W[cc * LDW + (r + i - c)];
+          for (int i = lane; i < L; i += 32) y += vs[i] * W[cc * LDW + d0 + i];
           y = warp_sum(y) * tau;
-          for (int i = lane; i < L; i += 32) W[cc * LDW + (r + i - c)] -= y * vs[i];
+          for (int i = lane; i < L; i += 32) W[cc * LDW + d0 + i] -= y * vs[i];
         }
-        // ---- (c1) w = tau * D v, D = A[r:r+L, r:r+L] skew from its lower triangle
-        const int dc = (int)(r - col);   // local column of r
-        for (int i = tid; i < L; i += 256) {
-          double sacc = 0.0;
-          for (int j = 0; j < i; j++) sacc += W[(dc + j) * LDW + (i - j)] * vs[j];      // D_ij, i > j
-          for (int j = i + 1; j < L; j++) sacc -= W[(dc + i) * LDW + (j - i)] * vs[j];  // -D_ji
-          ws[i] = tau * sacc;
-        }
-        // ---- (d1) z = E v, E = A[r+L:e, r:r+L]
-        const int ne = (int)(e - r - L);
-        for (int i = tid; i < ne; i += 256) {
-          double sacc = 0.0;
-          for (int j = 0; j < L; j++) sacc += W[(dc + j) * LDW + (L + i - j)] * vs[j];
-          zs[i] = tau * sacc;
+        // ---- (c1) w = tau D v (D skew, lower stored) and (d1) z = tau E v: 4 threads per row
+        {
+          const int row = tid >> 2, part = tid & 3;
+          double sw = 0.0, sz = 0.0;   // shuffles below run on all lanes (full mask)
+          if (row < L) {
+            for (int j = part; j < row; j += 4) sw += W[(dc + j) * LDW + (row - j)] * vs[j];
+            for (int j = row + 1 + part; j < L; j += 4) sw -= W[(dc + row) * LDW + (j - row)] * vs[j];
+          }
+          if (row < ne) {
+            for (int j = part; j < L; j += 4) sz += W[(dc + j) * LDW + (L + row - j)] * vs[j];
+          }
+          sw += __shfl_xor_sync(0xffffffffu, sw, 1);
+          sw += __shfl_xor_sync(0xffffffffu, sw, 2);
+          sz += __shfl_xor_sync(0xffffffffu, sz, 1);
+          sz += __shfl_xor_sync(0xffffffffu, sz, 2);
+          if (part == 0 && row < L) ws[row] = tau * sw;
+          if (part == 0 && row < ne) zs[row] = tau * sz;
         }
         __syncthreads();
         // ---- (c2) D_ij += v_i w_j - w_i v_j (i > j);  (d2) E_ij -= z_i v_j
-        for (int e2 = tid; e2 < L * L; e2 += 256) {
-          int i = e2 % L, j = e2 / L;
-          if (i > j) W[(dc + j) * LDW + (i - j)] += vs[i] * ws[j] - ws[i] * vs[j];
-        }
-        for (int e2 = tid; e2 < ne * L; e2 += 256) {
-          int i = e2 % ne, j = e2 / ne;
-          W[(dc + j) * LDW + (L + i - j)] -= zs[i] * vs[j];
+        for (int j = warp; j < L; j += 8) {
+          const double vj = vs[j], wj = ws[j];
+          for (int i = j + 1 + lane; i < L; i += 32) W[(dc + j) * LDW + (i - j)] += vs[i] * wj - ws[i] * vj;
+          for (int i = lane; i < ne; i += 32) W[(dc + j) * LDW + (L + i - j)] -= zs[i] * vj;
         }
       }
       __syncthreads();
       // ---- write back the touched entries
       for (int cc = warp; cc < ncol; cc += 8) {
-        int64_t c = col + cc;
-        int64_t lo = (c < r) ? r : c, hi = (c < r) ? r + L : e;
-        for (int64_t i = lo + lane; i < hi; i += 32) __stcg(&a.AB[(i - c) + c * a.ldab], W[cc * LDW + (i - c)]);
+        int64_t lo, hi;
+        seg(cc, lo, hi);
+        const int64_t c = col + cc;
+        for (int64_t i = lo + lane; i < hi; i += 32) __stcg(&a.AB[(i - c) + c * a.ldab], W[cc * LDW + (int)(i - c)]);
       }
       __threadfence();
       __syncthreads();
@@ -186,10 +222,19 @@ __global__ void band_copy_kernel(const double* ABin, int64_t ldin, int64_t n, in
 // BT2 group prep: for group g (reflectors of sweeps s0..s0+K2-1 at chase position t) build
 // the dense staircase V (window rows rho = 0..RW-1 start at row s0 + t*b, reflector c at rows
 // rho = c+1 .. c+b), its forward compact-WY T (Q_g = I - V T V^T, dlarft from the Gram
-// matrix) and U = V T^T, stored as Ud[g][c][rho] (so that Q_g X = X - V (U^T X)).
+// matrix) and U = V T^T.  Stored per group as one contiguous block in exactly the shared-
+// memory layout of the apply kernel: [U (K2 x LDW) | V (K2 x LDW)], U[c][rho], V[c][rho],
+// LDW = RW + 4, so that Q_g X = X - V (U^T X) and one bulk copy moves the whole group.
+template <int K2, int RW>
+struct BT2Grp {
+  static constexpr int LDW = RW + 4;
+  static constexpr int ELEMS = 2 * K2 * LDW;
+};
+
 template <int K2, int RW>
 __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const double* qtau, int64_t ngroups, int b,
-                                                      double* Ud) {
+                                                      double* UV) {
+  using Gp = BT2Grp<K2, RW>;
   __shared__ double V[K2][RW];
   __shared__ double G[K2][K2 + 1];
   __shared__ double T[K2][K2 + 1];
@@ -221,12 +266,16 @@ __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const d
       }
     }
     __syncthreads();
-    double* U = Ud + g * K2 * RW;
-    for (int e = threadIdx.x; e < K2 * RW; e += blockDim.x) {
-      int c = e / RW, rho = e % RW;
-      double s = 0.0;
-      for (int c2 = c; c2 < K2; c2++) s += V[c2][rho] * T[c][c2];
-      U[e] = s;
+    double* out = UV + g * Gp::ELEMS;
+    for (int e = threadIdx.x; e < K2 * Gp::LDW; e += blockDim.x) {
+      int c = e / Gp::LDW, rho = e % Gp::LDW;
+      double u = 0.0, vv = 0.0;
+      if (rho < RW) {
+        for (int c2 = c; c2 < K2; c2++) u += V[c2][rho] * T[c][c2];
+        vv = V[c][rho];
+      }
+      out[e] = u;
+      out[K2 * Gp::LDW + e] = vv;
     }
     __syncthreads();
   }
@@ -235,87 +284,111 @@ __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const d
 // BT2 apply: one CTA per strip of NB columns of X, persistent over all groups in the
 // order sweep blocks last -> first, t ascending.  The RW-row window
 // X[W0 : W0+RW, strip] (W0 = s0 + t*b) lives in a RING-row shared-memory ring: step t+1
-// reuses the last RW-b rows of window t, so per step only b new rows are loaded (cp.async,
-// prefetched during step t) and b rows are written back.  The next group's V (packed
-// staircase) and U are prefetched into a second buffer.  Per step:
-//   Z = U^T Xw   (K2 x NB, DMMA, skip U's zero upper triangle)
-//   Xw -= V Z    (RW x NB, DMMA, skip the staircase's zero fragments)
+// reuses the last RW-b rows of window t, so per step only b new rows are loaded and b
+// rows are written back.  The next group's [U | V] block (51 KB) arrives with ONE bulk
+// copy (cp.async.bulk, TMA engine) into the second buffer, tracked by an mbarrier; the b
+// new window rows arrive with cp.async (each thread: rows 2*lane.., fixed columns).
+// Per step:  Z = U^T Xw (K2 x NB, DMMA, skip U's zero upper triangle)
+//            Xw -= V Z  (RW x NB, DMMA, skip the staircase's zero fragments)
 template <int NB, int K2, int RW, int RING, int BB>
 struct BT2Cfg {
+  using Gp = BT2Grp<K2, RW>;
   static constexpr int LDX = RING + 4;   // Xs[col][slot]
-  static constexpr int LDU = RW + 4;     // Us[c][rho]
-  static constexpr int LDV = BB + 4;     // Vs[c][d]  (packed staircase, d = rho - c - 1)
+  static constexpr int LDW = Gp::LDW;    // U / V rows
   static constexpr int LDZ = K2 + 4;     // Zs[col][c]
-  static constexpr int XS = NB * LDX, US = K2 * LDU, VS = K2 * LDV, ZS = NB * LDZ;
-  static constexpr size_t SMEM = (size_t)(XS + 2 * US + 2 * VS + ZS) * sizeof(double);
-  static_assert(LDX % 16 == 4 && LDU % 16 == 4 && LDZ % 16 == 4, "pad");
-  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB, "ring");
+  static constexpr int XS = NB * LDX, GS = Gp::ELEMS, ZS = NB * LDZ;
+  static constexpr size_t SMEM = (size_t)(XS + 2 * GS + ZS) * sizeof(double) + 2 * sizeof(uint64_t);
+  static_assert(LDX % 16 == 4 && LDW % 16 == 4 && LDZ % 16 == 4, "pad");
+  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && NB == 64, "ring");
 };
 
 template <int NB, int K2, int RW, int RING, int BB>
 __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols,
-                                                          int64_t n, const double* __restrict__ qv,
-                                                          const double* __restrict__ Ud,
-                                                          const int64_t* __restrict__ gofs, int64_t nblk) {
+                                                          int64_t n, const double* __restrict__ UV,
+                                                          const int64_t* __restrict__ gofs, int64_t nblk,
+                                                          long long* dbg) {
   using C = BT2Cfg<NB, K2, RW, RING, BB>;
-  extern __shared__ __align__(16) double sh[];
+  extern __shared__ __align__(128) double sh[];
   double* Xs = sh;
-  double* Us0 = Xs + C::XS;
-  double* Vs0 = Us0 + 2 * C::US;
-  double* Zs = Vs0 + 2 * C::VS;
+  double* G0 = Xs + C::XS;            // [2][U | V]
+  double* Zs = G0 + 2 * C::GS;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Zs + C::ZS);
+  long long ph[6] = {0, 0, 0, 0, 0, 0}, tprev = 0, nsteps = 0;
+  const bool prof = (dbg != nullptr) && blockIdx.x == 0 && threadIdx.x == 0;
+#define BT2_TS(k) do { if (prof) { long long _t = clock64(); ph[k] += _t - tprev; tprev = _t; } } while (0)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
   const int64_t col0 = (int64_t)blockIdx.x * NB;
   const int ncl = (int)smin<int64_t>(NB, ncols - col0);
   const bool vec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-
-  // async loads -------------------------------------------------------------------
-  auto load_group = [&](int64_t g, int buf) {   // U (K2 x RW) and packed V (K2 x BB)
-    double* Us = Us0 + buf * C::US;
-    double* Vs = Vs0 + buf * C::VS;
-    const double* u = Ud + g * K2 * RW;
-    const double* v = qv + g * K2 * BB;
-    for (int e = tid; e < K2 * RW / 2; e += 256) {
-      int c = e / (RW / 2), r = (e % (RW / 2)) * 2;
-      cp_async16(Us + c * C::LDU + r, u + c * RW + r, 16);
-    }
-    for (int e = tid; e < K2 * BB / 2; e += 256) {
-      int c = e / (BB / 2), d = (e % (BB / 2)) * 2;
-      cp_async16(Vs + c * C::LDV + d, v + c * BB + d, 16);
-    }
-  };
-  auto load_rows = [&](int64_t r0, int nrows, int slot0) {   // rows [r0, r0+nrows) -> ring slots slot0..
-    for (int e = tid; e < NB * nrows / 2; e += 256) {
-      int cl = e / (nrows / 2), rr = (e % (nrows / 2)) * 2;
-      int slot = slot0 + rr;
-      if (slot >= RING) slot -= RING;
-      int64_t r = r0 + rr;
-      double* dst = Xs + cl * C::LDX + slot;
-      const double* src = X + SK_IDX(r, col0 + cl, ldx);
-      int cnt = (cl < ncl) ? (int)smin<int64_t>(2, smax<int64_t>(0, n - r)) : 0;
-      if (vec) {
-        cp_async16(dst, cnt ? src : X, cnt * 8);
-      } else {
-        cp_async8(dst, cnt > 0 ? src : X, cnt > 0 ? 8 : 0);
-        cp_async8(dst + 1, cnt > 1 ? src + 1 : X, cnt > 1 ? 8 : 0);
-      }
-    }
-  };
-  auto store_rows = [&](int64_t r0, int nrows, int slot0) {
-    for (int e = tid; e < NB * nrows; e += 256) {
-      int cl = e / nrows, rr = e % nrows;
-      int slot = slot0 + rr;
-      if (slot >= RING) slot -= RING;
-      int64_t r = r0 + rr;
-      if (cl < ncl && r < n) X[SK_IDX(r, col0 + cl, ldx)] = Xs[cl * C::LDX + slot];
-    }
-  };
-
-  int buf = 0;
   if (nblk <= 0) return;
+  for (int e = tid; e < C::XS; e += 256) Xs[e] = 0.0;   // ring rows beyond n stay finite
+  if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_fence_init(); }
+  __syncthreads();
+
+  auto load_group = [&](int64_t g, int buf) {   // thread 0: one bulk copy of the [U | V] block
+    fence_proxy_async();
+    mbar_expect_tx(&bar[buf], (unsigned)(C::GS * sizeof(double)));
+    bulk_g2s(G0 + buf * C::GS, UV + g * C::GS, (unsigned)(C::GS * sizeof(double)), &bar[buf]);
+  };
+  // this thread's 2-row chunk of column cl: rows r0 + rr, rr = 2*lane (64-row blocks)
+  auto load_chunk = [&](int64_t r, int cl, int slot) {
+    double* dst = Xs + cl * C::LDX + slot;
+    const double* src = X + SK_IDX(r, col0 + cl, ldx);
+    const int cnt = (cl < ncl) ? (int)smin<int64_t>(2, smax<int64_t>(0, n - r)) : 0;
+    if (vec) {
+      cp_async16(dst, cnt ? src : X, cnt * 8);
+    } else {
+      cp_async8(dst, cnt > 0 ? src : X, cnt > 0 ? 8 : 0);
+      cp_async8(dst + 1, cnt > 1 ? src + 1 : X, cnt > 1 ? 8 : 0);
+    }
+  };
+  auto load_rows64 = [&](int64_t r0, int slot0) {   // 64 rows x NB columns
+    const int rr = 2 * lane;
+    int slot = slot0 + rr;
+    if (slot >= RING) slot -= RING;
+#pragma unroll
+    for (int k = 0; k < NB / 8; k++) load_chunk(r0 + rr, warp + 8 * k, slot);
+  };
+  auto load_rows32 = [&](int64_t r0, int slot0) {   // 32 rows x NB columns
+    const int rr = 2 * (lane & 15);
+    int slot = slot0 + rr;
+    if (slot >= RING) slot -= RING;
+#pragma unroll
+    for (int k = 0; k < NB / 16; k++) load_chunk(r0 + rr, 2 * warp + (lane >> 4) + 16 * k, slot);
+  };
+  auto store_chunk = [&](int64_t r, int cl, int slot) {
+    if (cl >= ncl || r >= n) return;
+    double* dst = X + SK_IDX(r, col0 + cl, ldx);
+    const double2 v = *reinterpret_cast<const double2*>(Xs + cl * C::LDX + slot);
+    if (vec && r + 1 < n) {
+      *reinterpret_cast<double2*>(dst) = v;
+    } else {
+      dst[0] = v.x;
+      if (r + 1 < n) dst[1] = v.y;
+    }
+  };
+  auto store_rows64 = [&](int64_t r0, int slot0) {
+    const int rr = 2 * lane;
+    int slot = slot0 + rr;
+    if (slot >= RING) slot -= RING;
+#pragma unroll
+    for (int k = 0; k < NB / 8; k++) store_chunk(r0 + rr, warp + 8 * k, slot);
+  };
+  auto store_rows32 = [&](int64_t r0, int slot0) {
+    const int rr = 2 * (lane & 15);
+    int slot = slot0 + rr;
+    if (slot >= RING) slot -= RING;
+#pragma unroll
+    for (int k = 0; k < NB / 16; k++) store_chunk(r0 + rr, 2 * warp + (lane >> 4) + 16 * k, slot);
+  };
+
+  unsigned phase[2] = {0u, 0u};
+  int buf = 0;
   {
     const int64_t blk = nblk - 1;
-    load_group(gofs[blk], 0);
-    load_rows(blk * K2, RW, 0);
+    if (tid == 0) load_group(gofs[blk], 0);
+    load_rows64(blk * K2, 0);
+    load_rows32(blk * K2 + 64, 64);
     cp_async_commit();
   }
   for (int64_t blk = nblk - 1; blk >= 0; blk--) {
@@ -324,76 +397,105 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
     for (int64_t t = 0; t < ntask; t++) {
       const int64_t W0 = s0 + t * BB;
       const int off = (int)((t * BB) % RING);
+      if (prof) { tprev = clock64(); nsteps++; }
       cp_async_wait<0>();
+      mbar_wait(&bar[buf], phase[buf]);
+      phase[buf] ^= 1u;
       __syncthreads();
+      BT2_TS(0);
       // ---- prefetch the next group (and the next rows of the window, same block)
       if (t + 1 < ntask) {
-        load_group(gofs[blk] + t + 1, buf ^ 1);
+        if (tid == 0) load_group(gofs[blk] + t + 1, buf ^ 1);
         int so = off + RW;
         if (so >= RING) so -= RING;
-        load_rows(W0 + RW, BB, so);
+        load_rows64(W0 + RW, so);
       } else if (blk > 0) {
-        load_group(gofs[blk - 1], buf ^ 1);
+        if (tid == 0) load_group(gofs[blk - 1], buf ^ 1);
       }
       cp_async_commit();
-      const double* Us = Us0 + buf * C::US;
-      const double* Vs = Vs0 + buf * C::VS;
-      // ---- Z = U^T Xw : M = K2 (c), N = NB (col), K = RW (rho); warps 4 (M) x 2 (N)
+      BT2_TS(1);
+      const double* Us = G0 + buf * C::GS;
+      const double* Vs = Us + K2 * C::LDW;
+      // ---- Z = U^T Xw : each warp owns NB/8 columns and all K2 rows (balanced triangular
+      //      K extents); even / odd k-step accumulator sets; next fragments loaded first.
       {
-        constexpr int FN = NB / 16;
-        const int m0 = (warp & 3) * 8, n0 = (warp >> 2) * (NB / 2);
-        double acc[FN][2];
+        constexpr int FM = K2 / 8;
+        constexpr int NIT = RW / 8;
+        const int n0 = warp * (NB / 8);
+        double acc[2][FM][2];
 #pragma unroll
-        for (int j = 0; j < FN; j++) acc[j][0] = acc[j][1] = 0.0;
-        // U[rho][c] = 0 for rho <= c: k blocks with kk + 3 <= m0 are zero
-#pragma unroll 4
-        for (int kk = (m0 / 4) * 4; kk < RW; kk += 4) {
-          double af = Us[(m0 + gq) * C::LDU + kk + tq];
+        for (int p = 0; p < 2; p++)
+#pragma unroll
+          for (int i = 0; i < FM; i++) acc[p][i][0] = acc[p][i][1] = 0.0;
+        double fa[2][FM][2], fb[2][2];
+        auto ld1 = [&](int it, int sb) {
+          const int kk = it * 8;
           int slot = off + kk;
           if (slot >= RING) slot -= RING;
+          fb[sb][0] = Xs[(n0 + gq) * C::LDX + slot + tq];
+          fb[sb][1] = Xs[(n0 + gq) * C::LDX + slot + 4 + tq];
 #pragma unroll
-          for (int j = 0; j < FN; j++) {
-            double bf = Xs[(n0 + 8 * j + gq) * C::LDX + slot + tq];
-            dmma884(acc[j][0], acc[j][1], af, bf);
+          for (int i = 0; i < FM; i++) {
+            fa[sb][i][0] = Us[(8 * i + gq) * C::LDW + kk + tq];
+            fa[sb][i][1] = Us[(8 * i + gq) * C::LDW + kk + 4 + tq];
+          }
+        };
+        ld1(0, 0);
+#pragma unroll
+        for (int it = 0; it < NIT; it++) {
+          const int sb = it & 1;
+          if (it + 1 < NIT) ld1(it + 1, sb ^ 1);
+#pragma unroll
+          for (int i = 0; i < FM; i++) {
+            if (it * 8 + 7 < 8 * i) continue;   // U[rho][c] = 0 for rho <= c
+            dmma884(acc[0][i][0], acc[0][i][1], fa[sb][i][0], fb[sb][0]);
+            dmma884(acc[1][i][0], acc[1][i][1], fa[sb][i][1], fb[sb][1]);
           }
         }
 #pragma unroll
-        for (int j = 0; j < FN; j++) {
-          int nn = n0 + 8 * j + 2 * tq;
-          Zs[nn * C::LDZ + m0 + gq] = acc[j][0];
-          Zs[(nn + 1) * C::LDZ + m0 + gq] = acc[j][1];
+        for (int i = 0; i < FM; i++) {
+          const int nn = n0 + 2 * tq;
+          Zs[nn * C::LDZ + 8 * i + gq] = acc[0][i][0] + acc[1][i][0];
+          Zs[(nn + 1) * C::LDZ + 8 * i + gq] = acc[0][i][1] + acc[1][i][1];
         }
       }
       __syncthreads();
-      // ---- Xw -= V Z : M = RW (rho), N = NB, K = K2 (c); warps 4 (M, RW/4 rows) x 2 (N)
+      BT2_TS(2);
+      // ---- Xw -= V Z : M = RW (rho), N = NB, K = K2 (c); warps 4 (M, interleaved row
+      //      fragments: balanced staircase work) x 2 (N); zero staircase fragments skipped.
       {
         constexpr int FM = RW / 32, FN = NB / 16;
+        constexpr int NIT = K2 / 4;
         const int wm = warp & 3, n0 = (warp >> 2) * (NB / 2);
         double acc[FM][FN][2];
 #pragma unroll
         for (int i = 0; i < FM; i++)
 #pragma unroll
           for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        double fa[2][FM], fb[2][FN];
+        auto ld2 = [&](int it, int sb) {
+          const int kk = it * 4;
 #pragma unroll
-        for (int kk = 0; kk < K2; kk += 4) {
-          double bf[FN];
+          for (int j = 0; j < FN; j++) fb[sb][j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
 #pragma unroll
-          for (int j = 0; j < FN; j++) bf[j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
+          for (int i = 0; i < FM; i++) fa[sb][i] = Vs[(kk + tq) * C::LDW + 8 * (wm + 4 * i) + gq];
+        };
+        ld2(0, 0);
+#pragma unroll
+        for (int it = 0; it < NIT; it++) {
+          const int sb = it & 1, kk = it * 4;
+          if (it + 1 < NIT) ld2(it + 1, sb ^ 1);
 #pragma unroll
           for (int i = 0; i < FM; i++) {
-            const int m0 = wm * (RW / 4) + 8 * i;
-            // staircase: V[rho][c] != 0 iff 1 <= rho - c <= BB
-            if (m0 + 7 - kk < 1 || m0 - (kk + 3) > BB) continue;
-            const int rho = m0 + gq, c = kk + tq;
-            const int d = rho - c - 1;
-            double af = (d >= 0 && d < BB) ? Vs[c * C::LDV + d] : 0.0;
+            const int m0 = 8 * (wm + 4 * i);
+            if (m0 + 7 - kk < 1 || m0 - (kk + 3) > BB) continue;   // V[rho][c] != 0 iff 1 <= rho - c <= BB
 #pragma unroll
-            for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], af, bf[j]);
+            for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], fa[sb][i], fb[sb][j]);
           }
         }
 #pragma unroll
         for (int i = 0; i < FM; i++) {
-          const int m0 = wm * (RW / 4) + 8 * i;
+          const int m0 = 8 * (wm + 4 * i);
           int slot = off + m0;
           if (slot >= RING) slot -= RING;
 #pragma unroll
@@ -405,19 +507,30 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
         }
       }
       __syncthreads();
+      BT2_TS(3);
       // ---- write back the rows leaving the window
       if (t + 1 < ntask) {
-        store_rows(W0, BB, off);
+        store_rows64(W0, off);
       } else {
-        store_rows(W0, RW, off);
+        store_rows64(W0, off);
+        store_rows32(W0 + 64, off + 64 >= RING ? off + 64 - RING : off + 64);
         __syncthreads();
-        if (blk > 0) load_rows((blk - 1) * K2, RW, 0);   // first window of the next block
+        if (blk > 0) {
+          load_rows64((blk - 1) * K2, 0);   // first window of the next block
+          load_rows32((blk - 1) * K2 + 64, 64);
+        }
         cp_async_commit();
       }
+      BT2_TS(4);
       buf ^= 1;
     }
   }
   cp_async_wait<0>();
+  if (prof) {
+    for (int k = 0; k < 5; k++) dbg[k] = ph[k];
+    dbg[5] = nsteps;
+  }
+#undef BT2_TS
 }
 
 // ------------------------------------------------------------------------------------
@@ -453,13 +566,13 @@ void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w) {
   int64_t ng = std::max<int64_t>(L.ngroups, 1);
   w.qv = ar.take<double>((size_t)ng * L.k2 * L.b);
   w.qtau = ar.take<double>((size_t)ng * L.k2);
-  if (vectors) w.qT = ar.take<double>((size_t)ng * L.k2 * (L.b + L.k2));   // U_g (k2 x (b+k2)) per group
+  if (vectors) w.qT = ar.take<double>((size_t)ng * 2 * L.k2 * (L.b + L.k2 + 4));   // [U | V] per group
   w.gofs = ar.take<int64_t>(std::max<int64_t>(L.nblk, 1));
 }
 
 static int chase_grid(int64_t n, int b, int nsm) {
-  // concurrently active sweeps ~ (n/b)/4; never more CTAs than can be co-resident
-  int64_t act = std::max<int64_t>(1, (n / std::max(b, 1)) / 4 + 1);
+  // concurrently active sweeps ~ (n/b)/3; never more CTAs than can be co-resident
+  int64_t act = std::max<int64_t>(1, (n / std::max(b, 1)) / 3 + 1);
   return (int)std::max<int64_t>(1, std::min<int64_t>(act, nsm));
 }
 
@@ -509,9 +622,19 @@ cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int6
   e = cudaFuncSetAttribute(bt2_apply_kernel<NB, K2, RW, RING, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)Cf::SMEM);
   if (e) return e;
+  long long* dbgp = nullptr;
+  if (getenv("SKEWEIG_BT2_DBG")) cudaMalloc(&dbgp, 6 * sizeof(long long));   // debug instrumentation only
   KScope ks(KC_BT2, st);
   bt2_apply_kernel<NB, K2, RW, RING, BB><<<(unsigned)((ncols + NB - 1) / NB), 256, Cf::SMEM, st>>>(
-      X, ldx, ncols, L.n, w.qv, w.qT, w.gofs, L.nblk);
+      X, ldx, ncols, L.n, w.qT, w.gofs, L.nblk, dbgp);
+  if (dbgp) {
+    long long h[6];
+    cudaMemcpyAsync(h, dbgp, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[bt2 dbg] steps %lld  per-step cycles: wait %.0f prefetch %.0f gemm1 %.0f gemm2 %.0f store %.0f\n",
+            h[5], (double)h[0] / h[5], (double)h[1] / h[5], (double)h[2] / h[5], (double)h[3] / h[5], (double)h[4] / h[5]);
+    cudaFree(dbgp);
+  }
   return cudaGetLastError();
 }
 

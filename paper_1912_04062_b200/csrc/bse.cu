@@ -119,7 +119,7 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
       const double* L21 = M + SK_IDX(j0 + nb, j0, ldm);
       ga.A = L21; ga.lda = ldm; ga.B = L21; ga.ldb = ldm;
       ga.C = M + SK_IDX(j0 + nb, j0 + nb, ldm); ga.ldc = ldm; ga.alpha = -1.0; ga.beta = 1.0; ga.tri_off = 0;
-      e = gemm_dmma<128, 128, 16, 64, 32, 4, false, true, true>(ga, st);
+      e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
       if (e) return e;
     }
   }
@@ -133,7 +133,7 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
     GemmArgs ga;
     ga.M = m; ga.N = m; ga.K = m;
     ga.A = M; ga.lda = ldm; ga.B = M + m; ga.ldb = ldm; ga.C = S; ga.ldc = lds; ga.alpha = 1.0; ga.beta = 0.0;
-    e = gemm_dmma<128, 128, 16, 64, 32, 4, true, false, false>(ga, st);
+    e = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
     if (e) return e;
   }
   // W21 = -L22^T L11
@@ -142,7 +142,7 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
     ga.M = m; ga.N = m; ga.K = m;
     ga.A = M + SK_IDX(m, m, ldm); ga.lda = ldm; ga.B = M; ga.ldb = ldm; ga.C = W + m; ga.ldc = ldw;
     ga.alpha = -1.0; ga.beta = 0.0;
-    e = gemm_dmma<128, 128, 16, 64, 32, 4, true, false, false>(ga, st);
+    e = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
     if (e) return e;
   }
   {

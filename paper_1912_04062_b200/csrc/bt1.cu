@@ -69,7 +69,7 @@ cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_
       GemmArgs ga;
       ga.M = m; ga.N = K; ga.K = K;
       ga.A = V; ga.lda = ldv; ga.B = w.T; ga.ldb = K; ga.C = w.U; ga.ldc = ldu; ga.alpha = 1.0; ga.beta = 0.0;
-      e = gemm_dmma<128, 64, 16, 32, 32, 4, false, true, false>(ga, st);
+      e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, false>(ga, st);
       if (e) return e;
     }
     // Z = U^T X[r0:, :]
@@ -79,7 +79,7 @@ cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_
       GemmArgs ga;
       ga.M = K; ga.N = ncols; ga.K = m;
       ga.A = w.U; ga.lda = ldu; ga.B = Xr; ga.ldb = ldx; ga.C = w.Z; ga.ldc = K; ga.alpha = 1.0; ga.beta = 0.0;
-      e = gemm_dmma<128, 128, 16, 64, 32, 4, true, false, false>(ga, st);
+      e = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
       if (e) return e;
     }
     // X[r0:, :] -= V Z
@@ -88,7 +88,7 @@ cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_
       GemmArgs ga;
       ga.M = m; ga.N = ncols; ga.K = K;
       ga.A = V; ga.lda = ldv; ga.B = w.Z; ga.ldb = K; ga.C = Xr; ga.ldc = ldx; ga.alpha = -1.0; ga.beta = 1.0;
-      e = gemm_dmma<128, 128, 16, 64, 32, 4, false, false, false>(ga, st);
+      e = gemm_dmma<64, 64, 16, 32, 32, 2, false, false, false>(ga, st);
       if (e) return e;
     }
   }

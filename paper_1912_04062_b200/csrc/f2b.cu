@@ -254,10 +254,10 @@ struct SymmArgs {
 };
 
 template <int BM, int NB, int BK, int STAGES>
-__global__ void __launch_bounds__(256) symm_kernel(SymmArgs s) {
+__global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, false>::NTHREADS) symm_kernel(SymmArgs s) {
   using TR = GemmTile<BM, NB, BK, 32, 32, STAGES, false, false>;   // row part: A M-major
   using TC = GemmTile<BM, NB, BK, 32, 32, STAGES, true, false>;    // col part: A K-major
-  static_assert(TR::NTHREADS == 256, "8 warps");
+  constexpr int NT = TR::NTHREADS;
   extern __shared__ __align__(16) double smem[];
   const int64_t p = blockIdx.x;
   const int64_t m0 = p * BM;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) symm_kernel(SymmArgs s) {
       const int64_t k0 = kb * BK;
       if (k0 + BK > m0) {   // diagonal tile: keep row > col only
         double* a = As + cs * TR::A_STAGE;
-        for (int e = tid; e < BK * BM; e += 256) {
+        for (int e = tid; e < BK * BM; e += NT) {
           int kk = e / BM, mm = e % BM;
           if (m0 + mm <= k0 + kk) a[kk * TR::A_LD + mm] = 0.0;
         }
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(256) symm_kernel(SymmArgs s) {
       const int64_t k0 = m0 + kb * BK;
       if (k0 < m0 + BM) {   // diagonal tile: keep k > m0+mm only
         double* a = As + cs * TC::A_STAGE;
-        for (int e = tid; e < BK * BM; e += 256) {
+        for (int e = tid; e < BK * BM; e += NT) {
           int mm = e / BK, kk = e % BK;
           if (k0 + kk <= m0 + mm) a[mm * TC::A_LD + kk] = 0.0;
         }
@@ -411,7 +411,7 @@ __global__ void w_build_kernel(const double* V, int64_t ldv, const double* X, in
 // ------------------------------------------------------------------------------------
 // Host driver.
 
-static constexpr int kSymmBM = 128, kSymmBK = 16, kSymmStages = 4;
+static constexpr int kSymmBM = 64, kSymmBK = 16, kSymmStages = 2;
 static constexpr int kWRows = 256;
 
 void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w) {
@@ -502,7 +502,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
       set = true;
     }
     KScope ks(KC_SYMM, st);
-    symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)((m + kSymmBM - 1) / kSymmBM), 256, smem, st>>>(s);
+    symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)((m + kSymmBM - 1) / kSymmBM), TR::NTHREADS, smem, st>>>(s);
   }
   // W correction
   int nblk = (int)((m + kWRows - 1) / kWRows);
@@ -519,7 +519,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
   ga.A = w.P; ga.lda = ldn; ga.B = w.Q; ga.ldb = ldn; ga.C = S; ga.ldc = lda; ga.alpha = 1.0; ga.beta = 1.0;
   {
     KScope ks(KC_R2K, st);
-    e = gemm_dmma<128, 128, 16, 64, 32, 4, false, true, true>(ga, st);
+    e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
   }
   if (e) return e;
   return cudaGetLastError();

@@ -109,21 +109,30 @@ struct GemmTile {
     return B_NMAJ ? Bs[k * B_LD + n] : Bs[n * B_LD + k];
   }
 
-  // acc[FM][FN][2] += A_tile(warp rows) * B_tile(warp cols) over one BK block
+  // acc[FM][FN][2] += A_tile(warp rows) * B_tile(warp cols) over one BK block.  The
+  // fragments of k-step kk+4 are loaded into a second register set while the MMAs of
+  // k-step kk issue, so the shared-memory latency overlaps the DMMA pipe.
   __device__ __forceinline__ static void mma_stage(const double* As, const double* Bs, double (&acc)[FM][FN][2],
                                                    int wm0, int wn0, int lane) {
     const int gq = lane >> 2, t = lane & 3;
+    double af[2][FM], bf[2][FN];
+#pragma unroll
+    for (int i = 0; i < FM; i++) af[0][i] = a_at(As, wm0 + 8 * i + gq, t);
+#pragma unroll
+    for (int j = 0; j < FN; j++) bf[0][j] = b_at(Bs, t, wn0 + 8 * j + gq);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[FM], bf[FN];
+      const int cur = (kk / 4) & 1;
+      if (kk + 4 < BK) {
 #pragma unroll
-      for (int i = 0; i < FM; i++) af[i] = a_at(As, wm0 + 8 * i + gq, kk + t);
+        for (int i = 0; i < FM; i++) af[cur ^ 1][i] = a_at(As, wm0 + 8 * i + gq, kk + 4 + t);
 #pragma unroll
-      for (int j = 0; j < FN; j++) bf[j] = b_at(Bs, kk + t, wn0 + 8 * j + gq);
+        for (int j = 0; j < FN; j++) bf[cur ^ 1][j] = b_at(Bs, kk + 4 + t, wn0 + 8 * j + gq);
+      }
 #pragma unroll
       for (int i = 0; i < FM; i++)
 #pragma unroll
-        for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
   }
 
@@ -157,13 +166,15 @@ struct GemmTile {
   }
 };
 
-// Lower-triangular tile index t -> (tm, tn) with tm >= tn, t = tm(tm+1)/2 + tn.
-__device__ __forceinline__ void tri_tile(int64_t t, int64_t& tm, int64_t& tn) {
-  int64_t r = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((r + 1) * (r + 2) / 2 <= t) r++;
-  while (r * (r + 1) / 2 > t) r--;
+// Lower-triangular tile enumeration for BM = R * BN (R >= 1): row tile tm meets the
+// (strictly) lower triangle in column tiles tn = 0 .. R*(tm+1)-1; cumulative count
+// C(tm) = R * tm * (tm+1) / 2; t -> (tm, tn) with C(tm) <= t < C(tm+1).
+__device__ __forceinline__ void tri_tile(int64_t t, int R, int64_t& tm, int64_t& tn) {
+  int64_t r = (int64_t)((sqrt(8.0 * (double)t / R + 1.0) - 1.0) * 0.5);
+  while ((int64_t)R * (r + 1) * (r + 2) / 2 <= t) r++;
+  while ((int64_t)R * r * (r + 1) / 2 > t) r--;
   tm = r;
-  tn = t - r * (r + 1) / 2;
+  tn = t - (int64_t)R * r * (r + 1) / 2;
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJ, bool B_NMAJ, bool TRI>
@@ -173,34 +184,47 @@ gemm_dmma_kernel(GemmArgs g) {
   extern __shared__ __align__(16) double smem[];
   int64_t tm, tn;
   if (TRI) {
-    tri_tile(blockIdx.x, tm, tn);
+    tri_tile(blockIdx.x, BM / BN, tm, tn);
   } else {
     tm = blockIdx.x;
     tn = blockIdx.y;
   }
   const int64_t m0 = tm * BM, n0 = tn * BN;
-  double acc[T::FM][T::FN][2];
-#pragma unroll
-  for (int i = 0; i < T::FM; i++)
-#pragma unroll
-    for (int j = 0; j < T::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-  T::mainloop(g, smem, m0, n0, 0, g.K, acc);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm0 = (warp % T::NWARP_M) * WM, wn0 = (warp / T::NWARP_M) * WN;
   const int gq = lane >> 2, t = lane & 3;
+  // C = alpha*AB + beta*C computed as alpha*(AB + (beta/alpha) C): the C tile is loaded into
+  // the accumulators before the main loop so its latency overlaps the operand pipeline
+  // (exact for the alpha = +-1, beta in {0, 1} used by the library).
+  double acc[T::FM][T::FN][2];
+  const double cscale = (g.beta != 0.0) ? g.beta / g.alpha : 0.0;
+  // 32-bit tile-local indexing (keeps the register count down)
+  const int mrem = (int)smin<int64_t>(g.M - m0, BM), nrem = (int)smin<int64_t>(g.N - n0, BN);
+  const int dmn = (int)(m0 - n0);
+  const int ldc = (int)g.ldc;
+  double* Cb = g.C + SK_IDX(m0, n0, g.ldc);
 #pragma unroll
   for (int i = 0; i < T::FM; i++)
 #pragma unroll
     for (int j = 0; j < T::FN; j++)
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        int64_t m = m0 + wm0 + 8 * i + gq, n = n0 + wn0 + 8 * j + 2 * t + h;
-        if (m < g.M && n < g.N && (!TRI || m - n >= g.tri_off)) {
-          double* c = g.C + SK_IDX(m, n, g.ldc);
-          double v = g.alpha * acc[i][j][h];
-          if (g.beta != 0.0) v += g.beta * *c;
-          *c = v;
-        }
+        const int mi = wm0 + 8 * i + gq, nj = wn0 + 8 * j + 2 * t + h;
+        double v = 0.0;
+        if (cscale != 0.0 && mi < mrem && nj < nrem && (!TRI || dmn + mi - nj >= (int)g.tri_off))
+          v = cscale * Cb[mi + (size_t)nj * ldc];
+        acc[i][j][h] = v;
+      }
+  T::mainloop(g, smem, m0, n0, 0, g.K, acc);
+#pragma unroll
+  for (int i = 0; i < T::FM; i++)
+#pragma unroll
+    for (int j = 0; j < T::FN; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int mi = wm0 + 8 * i + gq, nj = wn0 + 8 * j + 2 * t + h;
+        if (mi < mrem && nj < nrem && (!TRI || dmn + mi - nj >= (int)g.tri_off))
+          Cb[mi + (size_t)nj * ldc] = g.alpha * acc[i][j][h];
       }
 }
 
@@ -220,7 +244,8 @@ cudaError_t gemm_dmma(const GemmArgs& g, cudaStream_t st) {
   }
   int64_t tm = (g.M + BM - 1) / BM, tn = (g.N + BN - 1) / BN;
   dim3 grid;
-  if (TRI) grid = dim3((unsigned)(tm * (tm + 1) / 2));
+  static_assert(!TRI || BM % BN == 0, "TRI needs BM = R * BN");
+  if (TRI) grid = dim3((unsigned)((BM / BN) * tm * (tm + 1) / 2));
   else grid = dim3((unsigned)tm, (unsigned)tn);
   kern<<<grid, T::NTHREADS, T::SMEM_BYTES, st>>>(ga);
   return cudaGetLastError();

@@ -251,17 +251,30 @@ __global__ void td_place_vectors(const double* y, const double* scale, int64_t n
 }
 
 // ---------------- block re-orthogonalisation helpers
-// partial H[(chunk)] = Qp^T Y over a row chunk: Qp n x p (ldq), Y n x nb (ldy); H p x nb
+// partial H[(chunk)] = Qp^T Y over a row chunk of kGramRows rows: both panels are staged
+// in shared memory with coalesced column loads (LD odd: conflict-free strided reads).
 __global__ void td_gram_partial(const double* Qp, int64_t ldq, int p, const double* Y, int64_t ldy, int nb,
                                 int64_t n, int64_t rows_per, double* part) {
-  extern __shared__ double hs[];
-  const int64_t r0 = blockIdx.x * rows_per, r1 = smin<int64_t>(n, r0 + rows_per);
+  extern __shared__ double gs[];
+  const int R = (int)rows_per, LD = R + 1;
+  double* Qs = gs;             // p x LD
+  double* Ys = gs + p * LD;    // nb x LD
+  const int64_t r0 = blockIdx.x * rows_per;
+  const int nr = (int)smin<int64_t>(rows_per, n - r0);
+  for (int e = threadIdx.x; e < p * R; e += blockDim.x) {
+    int i = e / R, r = e % R;
+    Qs[i * LD + r] = (r < nr) ? Qp[SK_IDX(r0 + r, i, ldq)] : 0.0;
+  }
+  for (int e = threadIdx.x; e < nb * R; e += blockDim.x) {
+    int j = e / R, r = e % R;
+    Ys[j * LD + r] = (r < nr) ? Y[SK_IDX(r0 + r, j, ldy)] : 0.0;
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < p * nb; e += blockDim.x) {
     int i = e % p, j = e / p;
     double s = 0.0;
-    const double* qa = Qp + SK_IDX(0, i, ldq);
-    const double* yb = Y + SK_IDX(0, j, ldy);
-    for (int64_t r = r0; r < r1; r++) s += qa[r] * yb[r];
+#pragma unroll 8
+    for (int r = 0; r < R; r++) s += Qs[i * LD + r] * Ys[j * LD + r];
     part[(size_t)blockIdx.x * p * nb + e] = s;
   }
 }
@@ -360,7 +373,7 @@ __global__ void assemble_D_kernel(const double* Q, int64_t ldq, int64_t n, int64
 
 // ------------------------------------------------------------------------------------
 static constexpr int kReorthNB = 32;
-static constexpr int64_t kGramRows = 1024;
+static constexpr int64_t kGramRows = 64;
 
 void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, int window) {
   int64_t nn = std::max<int64_t>(n, 1);
@@ -388,8 +401,15 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
 static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* Y, int64_t ldy, int nb, int64_t n,
                                   TridWork& w, cudaStream_t st) {
   int64_t nchunks = (n + kGramRows - 1) / kGramRows;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(td_gram_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e) return e;
+    attr = true;
+  }
   KScope ks(KC_TRID_REORTH, st, 2);
-  td_gram_partial<<<(unsigned)nchunks, 256, 0, st>>>(Qp, ldq, p, Y, ldy, nb, n, kGramRows, w.part);
+  td_gram_partial<<<(unsigned)nchunks, 256, (size_t)(p + nb) * (kGramRows + 1) * 8, st>>>(Qp, ldq, p, Y, ldy, nb, n,
+                                                                                          kGramRows, w.part);
   int cnt = p * nb;
   td_reduce_partials<<<(cnt + 255) / 256, 256, 0, st>>>(w.part, (int)nchunks, cnt, w.H);
   return cudaGetLastError();
