@@ -325,6 +325,10 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
   if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_fence_init(); }
   __syncthreads();
 
+  // Xs element (col, slot) lives at col*LDX + (slot ^ 4*bit2(col)): with LDX = 4 (mod 16) the
+  // GEMM1 B-fragment reads (8 columns x 4 slots) and the GEMM2 C read-modify-writes (4 column
+  // pairs x 8 slots) are both bank-conflict free.
+  auto xo = [&](int col, int slot) -> int { return col * C::LDX + (slot ^ (((col >> 2) & 1) << 2)); };
   auto load_group = [&](int64_t g, int buf) {   // thread 0: one bulk copy of the [U | V] block
     fence_proxy_async();
     mbar_expect_tx(&bar[buf], (unsigned)(C::GS * sizeof(double)));
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
   };
   // this thread's 2-row chunk of column cl: rows r0 + rr, rr = 2*lane (64-row blocks)
   auto load_chunk = [&](int64_t r, int cl, int slot) {
-    double* dst = Xs + cl * C::LDX + slot;
+    double* dst = Xs + xo(cl, slot);
     const double* src = X + SK_IDX(r, col0 + cl, ldx);
     const int cnt = (cl < ncl) ? (int)smin<int64_t>(2, smax<int64_t>(0, n - r)) : 0;
     if (vec) {
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
   auto store_chunk = [&](int64_t r, int cl, int slot) {
     if (cl >= ncl || r >= n) return;
     double* dst = X + SK_IDX(r, col0 + cl, ldx);
-    const double2 v = *reinterpret_cast<const double2*>(Xs + cl * C::LDX + slot);
+    const double2 v = *reinterpret_cast<const double2*>(Xs + xo(cl, slot));
     if (vec && r + 1 < n) {
       *reinterpret_cast<double2*>(dst) = v;
     } else {
@@ -416,28 +420,35 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
       BT2_TS(1);
       const double* Us = G0 + buf * C::GS;
       const double* Vs = Us + K2 * C::LDW;
-      // ---- Z = U^T Xw : each warp owns NB/8 columns and all K2 rows (balanced triangular
-      //      K extents); even / odd k-step accumulator sets; next fragments loaded first.
+      // ---- Z = U^T Xw : warps 2 (M: c fragments {h, h+2}, interleaved to balance U's zero
+      //      upper triangle) x 4 (N: NB/4 columns); even / odd k-step accumulator sets; next
+      //      fragments loaded before the current DMMAs.
       {
-        constexpr int FM = K2 / 8;
+        constexpr int FN = NB / 32;          // 2 column fragments per warp
         constexpr int NIT = RW / 8;
-        const int n0 = warp * (NB / 8);
-        double acc[2][FM][2];
+        const int h = warp & 1, n0 = (warp >> 1) * (NB / 4);
+        double acc[2][2][FN][2];
 #pragma unroll
         for (int p = 0; p < 2; p++)
 #pragma unroll
-          for (int i = 0; i < FM; i++) acc[p][i][0] = acc[p][i][1] = 0.0;
-        double fa[2][FM][2], fb[2][2];
+          for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < FN; j++) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
+        double fa[2][2][2], fb[2][FN][2];
         auto ld1 = [&](int it, int sb) {
           const int kk = it * 8;
           int slot = off + kk;
           if (slot >= RING) slot -= RING;
-          fb[sb][0] = Xs[(n0 + gq) * C::LDX + slot + tq];
-          fb[sb][1] = Xs[(n0 + gq) * C::LDX + slot + 4 + tq];
 #pragma unroll
-          for (int i = 0; i < FM; i++) {
-            fa[sb][i][0] = Us[(8 * i + gq) * C::LDW + kk + tq];
-            fa[sb][i][1] = Us[(8 * i + gq) * C::LDW + kk + 4 + tq];
+          for (int j = 0; j < FN; j++) {
+            fb[sb][j][0] = Xs[xo(n0 + 8 * j + gq, slot + tq)];
+            fb[sb][j][1] = Xs[xo(n0 + 8 * j + gq, slot + 4 + tq)];
+          }
+#pragma unroll
+          for (int i = 0; i < 2; i++) {
+            const int c = 8 * (h + 2 * i) + gq;
+            fa[sb][i][0] = Us[c * C::LDW + kk + tq];
+            fa[sb][i][1] = Us[c * C::LDW + kk + 4 + tq];
           }
         };
         ld1(0, 0);
@@ -446,18 +457,23 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
           const int sb = it & 1;
           if (it + 1 < NIT) ld1(it + 1, sb ^ 1);
 #pragma unroll
-          for (int i = 0; i < FM; i++) {
-            if (it * 8 + 7 < 8 * i) continue;   // U[rho][c] = 0 for rho <= c
-            dmma884(acc[0][i][0], acc[0][i][1], fa[sb][i][0], fb[sb][0]);
-            dmma884(acc[1][i][0], acc[1][i][1], fa[sb][i][1], fb[sb][1]);
+          for (int i = 0; i < 2; i++) {
+            if (it * 8 + 7 < 8 * (h + 2 * i)) continue;   // U[rho][c] = 0 for rho <= c
+#pragma unroll
+            for (int j = 0; j < FN; j++) {
+              dmma884(acc[0][i][j][0], acc[0][i][j][1], fa[sb][i][0], fb[sb][j][0]);
+              dmma884(acc[1][i][j][0], acc[1][i][j][1], fa[sb][i][1], fb[sb][j][1]);
+            }
           }
         }
 #pragma unroll
-        for (int i = 0; i < FM; i++) {
-          const int nn = n0 + 2 * tq;
-          Zs[nn * C::LDZ + 8 * i + gq] = acc[0][i][0] + acc[1][i][0];
-          Zs[(nn + 1) * C::LDZ + 8 * i + gq] = acc[0][i][1] + acc[1][i][1];
-        }
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+          for (int j = 0; j < FN; j++) {
+            const int c = 8 * (h + 2 * i) + gq, nn = n0 + 8 * j + 2 * tq;
+            Zs[nn * C::LDZ + c] = acc[0][i][j][0] + acc[1][i][j][0];
+            Zs[(nn + 1) * C::LDZ + c] = acc[0][i][j][1] + acc[1][i][j][1];
+          }
       }
       __syncthreads();
       BT2_TS(2);
@@ -501,8 +517,8 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
 #pragma unroll
           for (int j = 0; j < FN; j++) {
             int nn = n0 + 8 * j + 2 * tq;
-            Xs[nn * C::LDX + slot + gq] -= acc[i][j][0];
-            Xs[(nn + 1) * C::LDX + slot + gq] -= acc[i][j][1];
+            Xs[xo(nn, slot + gq)] -= acc[i][j][0];
+            Xs[xo(nn + 1, slot + gq)] -= acc[i][j][1];
           }
         }
       }
@@ -526,6 +542,275 @@ __global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ 
     }
   }
   cp_async_wait<0>();
+  if (prof) {
+    for (int k = 0; k < 5; k++) dbg[k] = ph[k];
+    dbg[5] = nsteps;
+  }
+#undef BT2_TS
+}
+
+// Warp-specialised BT2 apply (the default): 8 consumer warps run only the two DMMA tiles per
+// step; a 9th producer warp moves the data one step ahead -- it waits until the consumers
+// released step q-1 (mbarrier "empty"), writes that step's leaving rows back to X, then
+// loads step q+1's [U | V] block (one bulk TMA copy) and its new window rows (cp.async)
+// and signals mbarrier "full" (transaction bytes + cp.async completion arrivals).  The
+// ring offset advances by b per step inside a sweep block and by RW at a block boundary,
+// so the next block's first window never overlaps the window being computed.
+template <int NB, int K2, int RW, int RING, int BB>
+__global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols, int64_t n,
+                                                       const double* __restrict__ UV, const int64_t* __restrict__ gofs,
+                                                       int64_t nblk, long long* dbg) {
+  using C = BT2Cfg<NB, K2, RW, RING, BB>;
+  extern __shared__ __align__(128) double sh[];
+  double* Xs = sh;
+  double* G0 = Xs + C::XS;            // [2][U | V]
+  double* Zs = G0 + 2 * C::GS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Zs + C::ZS);
+  uint64_t* empty = full + 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  const int64_t col0 = (int64_t)blockIdx.x * NB;
+  const int ncl = (int)smin<int64_t>(NB, ncols - col0);
+  const bool vec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  if (nblk <= 0) return;
+  for (int e = tid; e < C::XS; e += blockDim.x) Xs[e] = 0.0;   // ring rows beyond n stay finite
+  if (tid == 0) {
+    mbar_init(&full[0], 128); mbar_init(&full[1], 128);
+    mbar_init(&empty[0], 8); mbar_init(&empty[1], 8);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto xo = [&](int col, int slot) -> int { return col * C::LDX + (slot ^ (((col >> 2) & 1) << 2)); };
+  auto ntask_of = [&](int64_t blk) -> int64_t { return 1 + (n - 3 - blk * K2) / BB; };
+
+  if (warp >= 8) {
+    // ============================ producer (4 warps) ============================
+    const int pw = warp - 8;                       // producer warp: columns pw, pw+4, ...
+    const int ptid = tid - 256;
+    auto load_rows = [&](int64_t r0, int cnt, int slot0) {   // rows [r0, r0+cnt) -> ring from slot0
+      for (int rr = 2 * lane; rr < cnt; rr += 64) {
+        int slot = slot0 + rr;
+        if (slot >= RING) slot -= RING;
+        const int64_t r = r0 + rr;
+        const int rc = (int)smin<int64_t>(2, smax<int64_t>(0, n - r));
+#pragma unroll 4
+        for (int cl = pw; cl < NB; cl += 4) {
+          double* dst = Xs + xo(cl, slot);
+          const int cnt2 = (cl < ncl) ? rc : 0;
+          const double* src = cnt2 ? X + SK_IDX(r, col0 + cl, ldx) : X;
+          if (vec) {
+            cp_async16(dst, src, cnt2 * 8);
+          } else {
+            cp_async8(dst, src, cnt2 > 0 ? 8 : 0);
+            cp_async8(dst + 1, cnt2 > 1 ? src + 1 : X, cnt2 > 1 ? 8 : 0);
+          }
+        }
+      }
+    };
+    auto store_rows = [&](int64_t r0, int cnt, int slot0) {
+      for (int rr = 2 * lane; rr < cnt; rr += 64) {
+        int slot = slot0 + rr;
+        if (slot >= RING) slot -= RING;
+        const int64_t r = r0 + rr;
+        if (r >= n) continue;
+#pragma unroll 4
+        for (int cl = pw; cl < NB; cl += 4) {
+          if (cl >= ncl) continue;
+          const double2 v = *reinterpret_cast<const double2*>(Xs + xo(cl, slot));
+          double* dst = X + SK_IDX(r, col0 + cl, ldx);
+          if (vec && r + 1 < n) {
+            *reinterpret_cast<double2*>(dst) = v;
+          } else {
+            dst[0] = v.x;
+            if (r + 1 < n) dst[1] = v.y;
+          }
+        }
+      }
+    };
+    auto load_group = [&](int64_t g, int b) {
+      if (ptid == 0) {
+        mbar_expect_tx_noarrive(&full[b], (unsigned)(C::GS * sizeof(double)));
+        fence_proxy_async();
+        bulk_g2s(G0 + b * C::GS, UV + g * C::GS, (unsigned)(C::GS * sizeof(double)), &full[b]);
+      }
+    };
+    // step 0
+    int64_t blk = nblk - 1, t = 0;
+    int off = 0;
+    load_group(gofs[blk], 0);
+    load_rows(blk * K2, RW, 0);
+    cp_async_mbar_arrive(&full[0]);
+    int64_t pblk = -1, pt = 0;
+    int poff = 0;
+    bool pstored = true;    // step q-1 already written back
+    for (int64_t q = 0;; q++) {
+      int64_t nblk_ = blk, nt = t + 1;
+      int noff = off + BB;
+      if (nt >= ntask_of(blk)) { nblk_ = blk - 1; nt = 0; noff = off + RW; }
+      if (noff >= RING) noff -= RING;
+      const bool has_next = nblk_ >= 0;
+      if (!pstored) {   // consumers released step q-1: write back its leaving rows
+        mbar_wait(&empty[(q - 1) & 1], (unsigned)(((q - 1) >> 1) & 1));
+        const bool pfinal = (pt + 1 >= ntask_of(pblk));
+        store_rows(pblk * K2 + pt * BB, pfinal ? RW : BB, poff);
+      }
+      bool stored = false;
+      if (has_next && nblk_ != blk && ntask_of(blk) == 1) {
+        // the next block's first window overlaps this single-step block's window:
+        // wait for step q and write it back before loading
+        mbar_wait(&empty[q & 1], (unsigned)((q >> 1) & 1));
+        store_rows(blk * K2 + t * BB, RW, off);
+        stored = true;
+      }
+      if (!has_next) {
+        if (!stored) {
+          mbar_wait(&empty[q & 1], (unsigned)((q >> 1) & 1));
+          store_rows(blk * K2 + t * BB, RW, off);
+        }
+        break;
+      }
+      {
+        const int b = (int)((q + 1) & 1);
+        load_group(gofs[nblk_] + nt, b);
+        if (nblk_ == blk) {
+          int so = noff + (RW - BB);
+          if (so >= RING) so -= RING;
+          load_rows(nblk_ * K2 + nt * BB + (RW - BB), BB, so);
+        } else {
+          load_rows(nblk_ * K2, RW, noff);
+        }
+        cp_async_mbar_arrive(&full[b]);
+      }
+      pblk = blk; pt = t; poff = off; pstored = stored;
+      blk = nblk_; t = nt; off = noff;
+    }
+    return;
+  }
+  // =============================== consumers ===============================
+  long long ph[6] = {0, 0, 0, 0, 0, 0}, tprev = 0, nsteps = 0;
+  const bool prof = (dbg != nullptr) && blockIdx.x == 0 && threadIdx.x == 0;
+#define BT2_TS(k) do { if (prof) { long long _t = clock64(); ph[k] += _t - tprev; tprev = _t; } } while (0)
+  int64_t blk = nblk - 1, t = 0;
+  int off = 0;
+  for (int64_t q = 0;; q++) {
+    if (prof) { tprev = clock64(); nsteps++; }
+    mbar_wait(&full[q & 1], (unsigned)((q >> 1) & 1));
+    BT2_TS(0);
+    const double* Us = G0 + (q & 1) * C::GS;
+    const double* Vs = Us + K2 * C::LDW;
+      // ---- Z = U^T Xw : warps 2 (M: c fragments {h, h+2}, interleaved to balance U's zero
+      //      upper triangle) x 4 (N: NB/4 columns); even / odd k-step accumulator sets; next
+      //      fragments loaded before the current DMMAs.
+      {
+        constexpr int FN = NB / 32;          // 2 column fragments per warp
+        constexpr int NIT = RW / 8;
+        const int h = warp & 1, n0 = (warp >> 1) * (NB / 4);
+        double acc[2][2][FN][2];
+#pragma unroll
+        for (int p = 0; p < 2; p++)
+#pragma unroll
+          for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < FN; j++) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
+        double fa[2][2][2], fb[2][FN][2];
+        auto ld1 = [&](int it, int sb) {
+          const int kk = it * 8;
+          int slot = off + kk;
+          if (slot >= RING) slot -= RING;
+#pragma unroll
+          for (int j = 0; j < FN; j++) {
+            fb[sb][j][0] = Xs[xo(n0 + 8 * j + gq, slot + tq)];
+            fb[sb][j][1] = Xs[xo(n0 + 8 * j + gq, slot + 4 + tq)];
+          }
+#pragma unroll
+          for (int i = 0; i < 2; i++) {
+            const int c = 8 * (h + 2 * i) + gq;
+            fa[sb][i][0] = Us[c * C::LDW + kk + tq];
+            fa[sb][i][1] = Us[c * C::LDW + kk + 4 + tq];
+          }
+        };
+        ld1(0, 0);
+#pragma unroll
+        for (int it = 0; it < NIT; it++) {
+          const int sb = it & 1;
+          if (it + 1 < NIT) ld1(it + 1, sb ^ 1);
+#pragma unroll
+          for (int i = 0; i < 2; i++) {
+            if (it * 8 + 7 < 8 * (h + 2 * i)) continue;   // U[rho][c] = 0 for rho <= c
+#pragma unroll
+            for (int j = 0; j < FN; j++) {
+              dmma884(acc[0][i][j][0], acc[0][i][j][1], fa[sb][i][0], fb[sb][j][0]);
+              dmma884(acc[1][i][j][0], acc[1][i][j][1], fa[sb][i][1], fb[sb][j][1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+          for (int j = 0; j < FN; j++) {
+            const int c = 8 * (h + 2 * i) + gq, nn = n0 + 8 * j + 2 * tq;
+            Zs[nn * C::LDZ + c] = acc[0][i][j][0] + acc[1][i][j][0];
+            Zs[(nn + 1) * C::LDZ + c] = acc[0][i][j][1] + acc[1][i][j][1];
+          }
+      }
+      named_bar(1 + (warp >> 2), 128);   // two independent 4-warp groups (columns 0-31 / 32-63)
+      BT2_TS(2);
+      // ---- Xw -= V Z : M = RW (rho), N = NB, K = K2 (c); warps 4 (M, interleaved row
+      //      fragments: balanced staircase work) x 2 (N); zero staircase fragments skipped.
+      {
+        constexpr int FM = RW / 32, FN = NB / 16;
+        constexpr int NIT = K2 / 4;
+        const int wm = warp & 3, n0 = (warp >> 2) * (NB / 2);
+        double acc[FM][FN][2];
+#pragma unroll
+        for (int i = 0; i < FM; i++)
+#pragma unroll
+          for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        double fa[2][FM], fb[2][FN];
+        auto ld2 = [&](int it, int sb) {
+          const int kk = it * 4;
+#pragma unroll
+          for (int j = 0; j < FN; j++) fb[sb][j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
+#pragma unroll
+          for (int i = 0; i < FM; i++) fa[sb][i] = Vs[(kk + tq) * C::LDW + 8 * (wm + 4 * i) + gq];
+        };
+        ld2(0, 0);
+#pragma unroll
+        for (int it = 0; it < NIT; it++) {
+          const int sb = it & 1, kk = it * 4;
+          if (it + 1 < NIT) ld2(it + 1, sb ^ 1);
+#pragma unroll
+          for (int i = 0; i < FM; i++) {
+            const int m0 = 8 * (wm + 4 * i);
+            if (m0 + 7 - kk < 1 || m0 - (kk + 3) > BB) continue;   // V[rho][c] != 0 iff 1 <= rho - c <= BB
+#pragma unroll
+            for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], fa[sb][i], fb[sb][j]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < FM; i++) {
+          const int m0 = 8 * (wm + 4 * i);
+          int slot = off + m0;
+          if (slot >= RING) slot -= RING;
+#pragma unroll
+          for (int j = 0; j < FN; j++) {
+            int nn = n0 + 8 * j + 2 * tq;
+            Xs[xo(nn, slot + gq)] -= acc[i][j][0];
+            Xs[xo(nn + 1, slot + gq)] -= acc[i][j][1];
+          }
+        }
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[q & 1]);
+    named_bar(1 + (warp >> 2), 128);   // two independent 4-warp groups (columns 0-31 / 32-63)
+    BT2_TS(3);
+    // advance
+    int64_t nt = t + 1;
+    int noff = off + BB;
+    if (nt >= ntask_of(blk)) { blk--; nt = 0; noff = off + RW; }
+    if (noff >= RING) noff -= RING;
+    if (blk < 0) break;
+    t = nt; off = noff;
+  }
   if (prof) {
     for (int k = 0; k < 5; k++) dbg[k] = ph[k];
     dbg[5] = nsteps;
@@ -624,9 +909,20 @@ cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int6
   if (e) return e;
   long long* dbgp = nullptr;
   if (getenv("SKEWEIG_BT2_DBG")) cudaMalloc(&dbgp, 6 * sizeof(long long));   // debug instrumentation only
-  KScope ks(KC_BT2, st);
-  bt2_apply_kernel<NB, K2, RW, RING, BB><<<(unsigned)((ncols + NB - 1) / NB), 256, Cf::SMEM, st>>>(
-      X, ldx, ncols, L.n, w.qT, w.gofs, L.nblk, dbgp);
+  const char* wsenv = getenv("SKEWEIG_BT2_WS");
+  const bool ws = !(wsenv && wsenv[0] == '0');
+  if (ws) {
+    const size_t smem = Cf::SMEM + 2 * sizeof(uint64_t);
+    e = cudaFuncSetAttribute(bt2_ws_kernel<NB, K2, RW, RING, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    KScope ks(KC_BT2, st);
+    bt2_ws_kernel<NB, K2, RW, RING, BB><<<(unsigned)((ncols + NB - 1) / NB), 384, smem, st>>>(
+        X, ldx, ncols, L.n, w.qT, w.gofs, L.nblk, dbgp);
+  } else {
+    KScope ks(KC_BT2, st);
+    bt2_apply_kernel<NB, K2, RW, RING, BB><<<(unsigned)((ncols + NB - 1) / NB), 256, Cf::SMEM, st>>>(
+        X, ldx, ncols, L.n, w.qT, w.gofs, L.nblk, dbgp);
+  }
   if (dbgp) {
     long long h[6];
     cudaMemcpyAsync(h, dbgp, sizeof(h), cudaMemcpyDeviceToHost, st);
