@@ -43,6 +43,8 @@ void F2BLayout::init(int64_t n_, int b_, int merge_) {
 // partial sums for column k+1 (||x[1:]||^2 and x[1:]^T P[:, c]) are produced in the
 // same pass that applies reflector k, and reduced in a fixed CTA order (bitwise
 // deterministic; every CTA derives identical beta/tau).
+static constexpr int kMaxPanelCTA = 152;   // >= max co-resident panel CTAs (148 SMs), multiple of 8
+
 struct PanelArgs {
   double* A; int64_t lda;      // panel P = A (m x kb), column-major, in place
   int64_t m; int kb;
@@ -107,8 +109,16 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
     const int buf = k & 1;
     // reduce partials over CTAs in a fixed order: warp w sums CTAs w, w+8, ...; then fixed combine
     for (int c = k + lane; c < kb; c += 32) {
+      // CTAs warp, warp+8, ...: all loads issued before the (fixed-order) sum
+      double v[kMaxPanelCTA / 8];
+#pragma unroll
+      for (int j = 0; j < kMaxPanelCTA / 8; j++) {
+        const int q = warp + 8 * j;
+        v[j] = (q < G) ? __ldcg(&a.part[((size_t)buf * G + q) * (kb + 1) + c]) : 0.0;
+      }
       double s = 0.0;
-      for (int q = warp; q < G; q += 8) s += __ldcg(&a.part[((size_t)buf * G + q) * (kb + 1) + c]);
+#pragma unroll
+      for (int j = 0; j < kMaxPanelCTA / 8; j++) s += v[j];
       red[warp * (kb + 1) + c] = s;
     }
     __syncthreads();
@@ -178,26 +188,44 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
       if (rb + li < kb && rb + li > c) a.A[SK_IDX(rb + li, c, a.lda)] = 0.0;
     }
   }
-  // Gram matrix G = V^T V (upper part), partial per CTA, fixed-order reduction
+  // Gram matrix G = V^T V, partial per CTA (4 x 4 register tile per thread), fixed-order
+  // reduction over CTAs, then T (forward columnwise dlarft) in shared memory by CTA 0.
   __syncthreads();
-  for (int e = tid; e < kb * kb; e += blockDim.x) {
-    int r = e % kb, c = e / kb;
-    double s = 0.0;
-    if (r < c) {
+  {
+    const int r0 = 4 * (tid % 16), c0 = 4 * (tid / 16);   // kb <= 64
+    double g4[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) g4[i][j] = 0.0;
+    if (r0 < kb && c0 < kb) {
       for (int li = 0; li < nr; li++) {
-        int64_t gi = rb + li;
-        double vr = (gi < r) ? 0.0 : (gi == r ? 1.0 : P(li, r));
-        double vc = (gi < c) ? 0.0 : (gi == c ? 1.0 : P(li, c));
-        s += vr * vc;
+        const int64_t gi = rb + li;
+        double vr[4], vc[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int r = r0 + i, c = c0 + i;
+          vr[i] = (r >= kb || gi < r) ? 0.0 : (gi == r ? 1.0 : P(li, r));
+          vc[i] = (c >= kb || gi < c) ? 0.0 : (gi == c ? 1.0 : P(li, c));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+          for (int j = 0; j < 4; j++) g4[i][j] += vr[i] * vc[j];
       }
     }
-    a.gram[(size_t)cta * kb * kb + e] = s;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (r0 + i < kb && c0 + j < kb) a.gram[(size_t)cta * kb * kb + (r0 + i) + (c0 + j) * kb] = g4[i][j];
   }
   __threadfence();
   grid.sync();
   double* gfin = a.gram + (size_t)G * kb * kb;
   for (int e = blockIdx.x * blockDim.x + tid; e < kb * kb; e += G * blockDim.x) {
     double s = 0.0;
+#pragma unroll 8
     for (int q = 0; q < G; q++) s += __ldcg(&a.gram[(size_t)q * kb * kb + e]);
     gfin[e] = s;
   }
@@ -205,35 +233,28 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
   grid.sync();
   // T (forward, columnwise dlarft): T[c][c] = tau_c, T[0:c, c] = -tau_c T[0:c,0:c] G[0:c, c]
   if (cta == 0) {
+    const int LDG = kb + 1;                 // odd: conflict-free row/column sweeps
+    double* Gs = sm;                        // kb x LDG  (the panel rows are no longer needed)
+    double* Ts = sm + kb * LDG;             // kb x LDG
+    for (int e = tid; e < kb * kb; e += blockDim.x) {
+      const int l = e % kb, c = e / kb;
+      Gs[l * LDG + c] = __ldcg(&gfin[e]);
+      Ts[l * LDG + c] = 0.0;
+    }
+    __syncthreads();
     for (int r = tid; r < kb; r += blockDim.x) {
-      double trow[128];
-      for (int c = 0; c < kb; c++) trow[c] = 0.0;
-      trow[r] = __ldcg(&a.tau[r]);
+      Ts[r * LDG + r] = __ldcg(&a.tau[r]);
       for (int c = r + 1; c < kb; c++) {
         double s = 0.0;
-        for (int l = r; l < c; l++) s += trow[l] * __ldcg(&gfin[l + c * kb]);
-        trow[c] = -__ldcg(&a.tau[c]) * s;
+        for (int l = r; l < c; l++) s += Ts[r * LDG + l] * Gs[l * LDG + c];
+        Ts[r * LDG + c] = -__ldcg(&a.tau[c]) * s;
       }
-      for (int c = 0; c < kb; c++) a.T[r + c * a.ldt] = trow[c];
     }
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// U = V T  (m x kb), one thread per row; T staged in shared memory.
-__global__ void vt_kernel(const double* V, int64_t ldv, const double* T, int ldt, int64_t m, int kb,
-                          double* U, int64_t ldu) {
-  extern __shared__ double Ts[];
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) Ts[e] = T[(e % kb) + (e / kb) * ldt];
-  __syncthreads();
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  double v[128];
-  for (int a = 0; a < kb; a++) v[a] = V[SK_IDX(i, a, ldv)];
-  for (int c = 0; c < kb; c++) {
-    double s = 0.0;
-    for (int a = 0; a <= c; a++) s += v[a] * Ts[a + c * kb];
-    U[SK_IDX(i, c, ldu)] = s;
+    __syncthreads();
+    for (int e = tid; e < kb * kb; e += blockDim.x) {
+      const int r = e % kb, c = e / kb;
+      a.T[r + c * a.ldt] = Ts[r * LDG + c];
+    }
   }
 }
 
@@ -359,52 +380,65 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
 }
 
 // ------------------------------------------------------------------------------------
-// a4 W correction.  (1) per row-block partial Z_blk = V_blk^T X_blk (kb x kb)
-__global__ void vtx_partial_kernel(const double* V, int64_t ldv, const double* X, int64_t ldx, int64_t m, int kb,
-                                   int rows_per_blk, double* part) {
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk;
-  const int64_t r1 = smin<int64_t>(m, r0 + rows_per_blk);
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    int a = e % kb, c = e / kb;
-    double s = 0.0;
-    for (int64_t i = r0; i < r1; i++) s += V[SK_IDX(i, a, ldv)] * X[SK_IDX(i, c, ldx)];
-    part[(size_t)blockIdx.x * kb * kb + e] = s;
-  }
+// a4 W correction, W = X - 1/2 V (T^T (V^T X))  (Eq. (7)):
+// (1) per 256-row chunk: partial Z_chunk = V_chunk^T X_chunk (64 x 64, DMMA tiles)
+template <int BK>
+__global__ void __launch_bounds__(128) vtx_partial_kernel(const double* V, int64_t ldv, const double* X, int64_t ldx,
+                                                          int64_t m, int rows_per_chunk, double* part) {
+  using T = GemmTile<64, 64, BK, 32, 32, 2, true, false>;
+  extern __shared__ __align__(16) double smem[];
+  GemmArgs g;
+  g.M = 64; g.N = 64; g.K = m;
+  g.A = V; g.lda = ldv; g.B = X; g.ldb = ldx;
+  g.vec = gemm_vec_ok(V, ldv, X, ldx) ? 1 : 0;
+  double acc[T::FM][T::FN][2];
+#pragma unroll
+  for (int i = 0; i < T::FM; i++)
+#pragma unroll
+    for (int j = 0; j < T::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int64_t k0 = (int64_t)blockIdx.x * rows_per_chunk;
+  T::mainloop(g, smem, 0, 0, k0, smin<int64_t>(m, k0 + rows_per_chunk), acc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm0 = (warp % T::NWARP_M) * 32, wn0 = (warp / T::NWARP_M) * 32;
+  const int gq = lane >> 2, t = lane & 3;
+  double* out = part + (size_t)blockIdx.x * 64 * 64;
+#pragma unroll
+  for (int i = 0; i < T::FM; i++)
+#pragma unroll
+    for (int j = 0; j < T::FN; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) out[(wm0 + 8 * i + gq) + (wn0 + 8 * j + 2 * t + h) * 64] = acc[i][j][h];
 }
-// (2) Z = sum of partials (fixed order); Mb = T^T Z; writes Mb (kb x kb)
-__global__ void mb_kernel(const double* part, int nblk, const double* T, int ldt, int kb, double* Mb) {
-  extern __shared__ double zs[];
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < nblk; q++) s += part[(size_t)q * kb * kb + e];
-    zs[e] = s;
-  }
+// (2) Z = sum of the chunk partials (fixed order, loads in flight), one element per thread
+__global__ void zsum_kernel(const double* part, int nchunk, int cnt, double* Z) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cnt) return;
+  double s = 0.0;
+#pragma unroll 8
+  for (int q = 0; q < nchunk; q++) s += part[(size_t)q * cnt + e];
+  Z[e] = s;
+}
+// (3) Mb = T^T Z (kb x kb, T upper), one CTA
+__global__ void mb_kernel(const double* Z, const double* T, int ldt, int kb, double* Mb) {
+  extern __shared__ double zs[];   // kb x kb (T is read through L1/L2)
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) zs[e] = Z[e];
   __syncthreads();
   for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    int a = e % kb, c = e / kb;
+    const int a = e % kb, c = e / kb;
     double s = 0.0;
-    for (int l = 0; l <= a; l++) s += T[l + a * ldt] * zs[l + c * kb];   // (T^T)_{a l} = T_{l a}, T upper
+    for (int l = 0; l <= a; l++) s += T[l + a * ldt] * zs[l + c * kb];   // (T^T)_{a l} = T_{l a}
     Mb[e] = s;
   }
 }
-// (3) W = X - 1/2 V Mb ; P = [V W], Q = [W -V]  (m x 2kb each, ld = ldp)
-__global__ void w_build_kernel(const double* V, int64_t ldv, const double* X, int64_t ldx, const double* Mb,
-                               int64_t m, int kb, double* P, double* Q, int64_t ldp) {
-  extern __shared__ double ms[];
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) ms[e] = Mb[e];
-  __syncthreads();
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  double v[128];
-  for (int a = 0; a < kb; a++) v[a] = V[SK_IDX(i, a, ldv)];
-  for (int c = 0; c < kb; c++) {
-    double s = 0.0;
-    for (int a = 0; a < kb; a++) s += v[a] * ms[a + c * kb];
-    double w = X[SK_IDX(i, c, ldx)] - 0.5 * s;
-    P[SK_IDX(i, c, ldp)] = v[c];
-    P[SK_IDX(i, kb + c, ldp)] = w;
+// (4) P = [V W], Q = [W -V] with W already in P[:, kb:2kb]
+__global__ void pq_build_kernel(const double* V, int64_t ldv, int64_t m, int kb, double* P, double* Q, int64_t ldp) {
+  const int64_t c = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = V[SK_IDX(i, c, ldv)];
+    const double w = P[SK_IDX(i, kb + c, ldp)];
+    P[SK_IDX(i, c, ldp)] = v;
     Q[SK_IDX(i, c, ldp)] = w;
-    Q[SK_IDX(i, kb + c, ldp)] = -v[c];
+    Q[SK_IDX(i, kb + c, ldp)] = -v;
   }
 }
 
@@ -427,7 +461,7 @@ void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w) {
   w.X = ar.take<double>(ldn * b);
   w.P = ar.take<double>(ldn * 2 * b);
   w.Q = ar.take<double>(ldn * 2 * b);
-  w.zpart = ar.take<double>(((n + kWRows - 1) / kWRows + 1) * b * b);
+  w.zpart = ar.take<double>(((n + kWRows - 1) / kWRows + 2) * b * b);
   w.Mb = ar.take<double>(b * b);
 }
 
@@ -450,8 +484,10 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   int G = panel_grid(m, nsm);
   a.R = (m + G - 1) / G;
   size_t extra = (size_t)(8 * (b + 1) + (b + 1) + b + 4) * sizeof(double);
-  size_t smem_full = (size_t)b * a.R * sizeof(double) + extra;
-  bool use_smem = smem_full <= 200 * 1024;
+  const size_t tbuild = (size_t)2 * b * (b + 1) * sizeof(double);   // CTA 0's G and T in the T build
+  size_t smem_full = std::max((size_t)b * a.R * sizeof(double), tbuild) + extra;
+  bool use_smem = (size_t)b * a.R * sizeof(double) + extra <= 200 * 1024;
+  if (!use_smem) extra = std::max(extra, tbuild);
   a.smem_rows = use_smem ? (int)a.R : 0;
   void* args[] = {&a};
   cudaError_t e;
@@ -465,6 +501,8 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
     }
     e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel<true>, dim3(G), dim3(256), args, smem_full, st);
   } else {
+    e = cudaFuncSetAttribute(panel_qr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)extra);
+    if (e) return e;
     e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel<false>, dim3(G), dim3(256), args, extra, st);
   }
   return e;
@@ -480,16 +518,19 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
   const double* Tj = w.T + j * (int64_t)b * b;
   const int64_t ldn = (m + 1) & ~int64_t(1);
   double* S = A + SK_IDX(r0, r0, lda);
+  double* Wp = w.P + ldn * b;   // X, then W, lives in P[:, b:2b]
   cudaError_t e;
-  // U = V T
-  {
+  {   // U = V T  (m x b)
     KScope ks(KC_VT, st);
-    vt_kernel<<<(unsigned)((m + 127) / 128), 128, b * b * sizeof(double), st>>>(Vj, ldv, Tj, b, m, b, w.U, ldn);
+    GemmArgs ga;
+    ga.M = m; ga.N = b; ga.K = b;
+    ga.A = Vj; ga.lda = ldv; ga.B = Tj; ga.ldb = b; ga.C = w.U; ga.ldc = ldn; ga.alpha = 1.0; ga.beta = 0.0;
+    e = gemm_dmma<64, 64, 16, 32, 32, 2, false, false, false>(ga, st);
+    if (e) return e;
   }
-  // X = S U
-  {
+  {   // X = S U  -> P[:, b:2b]
     SymmArgs s;
-    s.S = S; s.lds = lda; s.U = w.U; s.ldu = ldn; s.X = w.X; s.ldx = ldn; s.m = m; s.nb = b;
+    s.S = S; s.lds = lda; s.U = w.U; s.ldu = ldn; s.X = Wp; s.ldx = ldn; s.m = m; s.nb = b;
     s.vec = gemm_vec_ok(S, lda, w.U, ldn) ? 1 : 0;
     using TR = GemmTile<kSymmBM, 64, kSymmBK, 32, 32, kSymmStages, false, false>;
     using TC = GemmTile<kSymmBM, 64, kSymmBK, 32, 32, kSymmStages, true, false>;
@@ -504,14 +545,21 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     KScope ks(KC_SYMM, st);
     symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)((m + kSymmBM - 1) / kSymmBM), TR::NTHREADS, smem, st>>>(s);
   }
-  // W correction
-  int nblk = (int)((m + kWRows - 1) / kWRows);
-  {
-  KScope ks(KC_WCORR, st, 3);
-  vtx_partial_kernel<<<nblk, 256, 0, st>>>(Vj, ldv, w.X, ldn, m, b, kWRows, w.zpart);
-  mb_kernel<<<1, 256, b * b * sizeof(double), st>>>(w.zpart, nblk, Tj, b, b, w.Mb);
-  w_build_kernel<<<(unsigned)((m + 127) / 128), 128, b * b * sizeof(double), st>>>(Vj, ldv, w.X, ldn, w.Mb, m, b,
-                                                                                     w.P, w.Q, ldn);
+  {   // W = X - 1/2 V (T^T (V^T X));  P = [V W], Q = [W -V]
+    KScope ks(KC_WCORR, st, 5);
+    const int nchunk = (int)((m + kWRows - 1) / kWRows);
+    using TV = GemmTile<64, 64, 16, 32, 32, 2, true, false>;
+    vtx_partial_kernel<16><<<nchunk, 128, TV::SMEM_BYTES, st>>>(Vj, ldv, Wp, ldn, m, kWRows, w.zpart);
+    double* Zr = w.zpart + (size_t)nchunk * b * b;
+    zsum_kernel<<<(b * b + 255) / 256, 256, 0, st>>>(w.zpart, nchunk, b * b, Zr);
+    mb_kernel<<<1, 256, b * b * sizeof(double), st>>>(Zr, Tj, b, b, w.Mb);
+    GemmArgs ga;
+    ga.M = m; ga.N = b; ga.K = b;
+    ga.A = Vj; ga.lda = ldv; ga.B = w.Mb; ga.ldb = b; ga.C = Wp; ga.ldc = ldn; ga.alpha = -0.5; ga.beta = 1.0;
+    e = gemm_dmma<64, 64, 16, 32, 32, 2, false, false, false>(ga, st);
+    if (e) return e;
+    dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 32), (unsigned)b);
+    pq_build_kernel<<<grid, 256, 0, st>>>(Vj, ldv, m, b, w.P, w.Q, ldn);
   }
   // S_lower += P Q^T
   GemmArgs ga;

@@ -31,7 +31,7 @@ struct GemmArgs {
 };
 
 // true when both operands allow 16-byte (2 x double) vector copies
-inline bool gemm_vec_ok(const void* A, int64_t lda, const void* B, int64_t ldb) {
+__host__ __device__ inline bool gemm_vec_ok(const void* A, int64_t lda, const void* B, int64_t ldb) {
   return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 && (lda % 2 == 0) &&
          (ldb % 2 == 0);
 }
