@@ -37,24 +37,35 @@ struct ChaseArgs {
   double* qv;                   // reflector store: [group][k2][b]
   double* qtau;                 // [group][k2]
   const int64_t* gofs;          // [nblk] first group index of each sweep block
+  long long* dbg;               // optional instrumentation (SKEWEIG_CHASE_DBG)
 };
 
 __device__ __forceinline__ int64_t chase_ntask(int64_t n, int b, int64_t s) { return 1 + (n - 3 - s) / b; }
 
 template <int MAXB>
 __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
-  extern __shared__ __align__(16) double W[];     // window [2b cols][LDW]
-  __shared__ double vs[MAXB], ws[MAXB], zs[MAXB], sc[4];
+  // Shared window: a ring of 2b column slots (+1 for the t = 0 column) in band storage,
+  // slot(c) = (c - s - 1) mod 2b.  Task t of sweep s works on columns [r-b, r+b); the
+  // block below its diagonal block (E_t, rows [r+L, e)) is exactly task t+1's left block,
+  // so it stays in shared memory (loaded once, written back once, as task t+1's final
+  // left block); each task loads only its diagonal-block columns [r, r+L) and writes back
+  // its (final) left block and diagonal block.
+  extern __shared__ __align__(16) double W[];
+  __shared__ double vs[MAXB], ws[MAXB], zs[MAXB], ys[MAXB], sc[4];
   const int b = a.b;
   const int LDW = 2 * b + 2;   // LDW - 1 odd: the strided skew reads of D are conflict-free
   const int64_t n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool prof = a.dbg != nullptr && blockIdx.x == 0 && tid == 0;
+  long long t_wait = 0, t_work = 0, ntasks = 0, tk = 0, tph[5] = {0, 0, 0, 0, 0}, tp = 0;
+#define CH_TS(i) do { if (prof) { long long _n = clock64(); tph[i] += _n - tp; tp = _n; } } while (0)
   for (int64_t s = blockIdx.x; s < n - 2; s += gridDim.x) {
     const int64_t nt = chase_ntask(n, b, s);
     const int64_t ntprev = (s > 0) ? chase_ntask(n, b, s - 1) : 0;
     for (int64_t t = 0; t < nt; t++) {
       // ---- sweep s task t may run once sweep s-1 finished tasks 0..t+2 (their entry sets
       //      are then disjoint from this task's; checked against the sequential order)
+      if (prof) tk = clock64();
       if (s > 0) {
         if (tid == 0) {
           const int need = (int)smin<int64_t>(t + 3, ntprev);
@@ -64,58 +75,45 @@ __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
         }
         __syncthreads();
       }
+      if (prof) { long long now = clock64(); t_wait += now - tk; tk = now; tp = now; ntasks++; }
       int64_t col, r, L;
       if (t == 0) { col = s; r = s + 1; L = smin<int64_t>(b, n - 1 - s); }
       else { col = s + 1 + (t - 1) * b; r = col + b; L = smin<int64_t>(b, n - r); }
       const int64_t e = smin<int64_t>(n, r + L + b);
-      const int ncol = (int)(r + L - col);
       const int nl = (int)(r - col);          // columns of the left block (1 for t = 0)
       const int ne = (int)(e - r - L);         // rows of the block below
-      const int dc = nl;                       // local column of r
-      // ---- load the touched entries: column cc (warp-strided) has rows [lo, hi) with
-      //      lo = r, hi = r+L for the left columns (c < r) and lo = c, hi = e otherwise.
-      //      Two columns x four rows per lane are loaded (L2-coherent __ldcg) before any
-      //      shared store, so eight loads are in flight per thread.
-      auto seg = [&](int cc, int64_t& lo, int64_t& hi) {
-        const int64_t c = col + cc;
-        lo = (c < r) ? r : c;
-        hi = (c < r) ? r + L : e;
-      };
-      for (int cc0 = warp; cc0 < ncol; cc0 += 16) {
-        double v[2][4];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int cc = cc0 + 8 * h;
-          int64_t lo = 0, hi = 0;
-          if (cc < ncol) seg(cc, lo, hi);
-          const int64_t c = col + cc;
-#pragma unroll
-          for (int k = 0; k < 4; k++) {
-            const int64_t i = lo + lane + 32 * k;
-            v[h][k] = (cc < ncol && i < hi) ? __ldcg(&a.AB[(i - c) + c * a.ldab]) : 0.0;
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int cc = cc0 + 8 * h;
-          if (cc >= ncol) continue;
-          int64_t lo, hi;
-          seg(cc, lo, hi);
-          const int64_t c = col + cc;
-#pragma unroll
-          for (int k = 0; k < 4; k++) {
-            const int64_t i = lo + lane + 32 * k;
-            if (i < hi) W[cc * LDW + (int)(i - c)] = v[h][k];
-          }
-        }
+      const bool last = (t + 1 == nt);
+      // column slots (32-bit, no division in the inner loops): left columns col + cc, and
+      // the diagonal-block columns r + j
+      const int B2 = 2 * b;
+      const int sr0 = (int)((r - s - 1) % B2);
+      const int sc0 = (t == 0) ? B2 : (int)((col - s - 1) % B2);
+      auto sl_left = [&](int cc) -> int { if (t == 0) return B2; int x = sc0 + cc; return x >= B2 ? x - B2 : x; };
+      auto sl_diag = [&](int j) -> int { int x = sr0 + j; return x >= B2 ? x - B2 : x; };
+      // ---- load: t = 0 also the left column s; always the columns [r, r+L) rows [c, e).
+      //      16-byte L2-coherent cp.async on even-widened band offsets (widened elements
+      //      are only read, never written back).
+      if (t == 0 && warp == 7) {
+        const int d0 = (int)(r - col) & ~1, d1 = (int)(r + L - col);
+        for (int d = d0 + 2 * lane; d < d1; d += 64) cp_async16(&W[B2 * LDW + d], &a.AB[d + col * a.ldab], 16);
       }
+      for (int j = warp; j < L; j += 8) {
+        const int64_t c = r + j;
+        const int d1 = (int)(e - c);
+        const int sj = sl_diag(j);
+        for (int d = 2 * lane; d < d1; d += 64) cp_async16(&W[sj * LDW + d], &a.AB[d + c * a.ldab], 16);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
       __syncthreads();
+      CH_TS(0);
       // ---- (a) Householder of x = A[r:r+L, col]  (dlarfg convention)
+      const int scol = sl_left(0);
       if (warp == 0) {
         double s2 = 0.0;
-        for (int i = 1 + lane; i < L; i += 32) { double x = W[(r + i - col)]; s2 += x * x; }
+        for (int i = 1 + lane; i < L; i += 32) { double x = W[scol * LDW + (r + i - col)]; s2 += x * x; }
         s2 = warp_sum(s2);
-        double x0 = W[(r - col)];
+        double x0 = W[scol * LDW + (r - col)];
         double beta, tau, scal;
         if (s2 == 0.0) { beta = x0; tau = 0.0; scal = 0.0; }
         else {
@@ -125,13 +123,14 @@ __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
           scal = 1.0 / (x0 - beta);
         }
         for (int i = lane; i < L; i += 32) {
-          double v = (i == 0) ? 1.0 : W[(r + i - col)] * scal;
+          double v = (i == 0) ? 1.0 : W[scol * LDW + (r + i - col)] * scal;
           vs[i] = v;
-          W[(r + i - col)] = (i == 0) ? beta : 0.0;
+          W[scol * LDW + (r + i - col)] = (i == 0) ? beta : 0.0;
         }
         if (lane == 0) sc[0] = tau;
       }
       __syncthreads();
+      CH_TS(1);
       const double tau = sc[0];
       {   // store the reflector (v zero-padded to b by the initial memset)
         const int64_t blk = s / a.k2, c = s % a.k2;
@@ -141,56 +140,82 @@ __global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
         if (tid == 0) a.qtau[gidx * a.k2 + c] = tau;
       }
       if (tau != 0.0) {
-        // ---- (b) left block columns (col, r): y = tau v^T A[r:r+L, c]; A -= v y   (warp per column)
-        for (int cc = 1 + warp; cc < nl; cc += 8) {
-          const int d0 = nl - cc;   // row r sits at offset r - c = nl - cc
-          double y = 0.0;
-          for (int i = lane; i < L; i += 32) y += vs[i] * W[cc * LDW + d0 + i];
-          y = warp_sum(y) * tau;
-          for (int i = lane; i < L; i += 32) W[cc * LDW + d0 + i] -= y * vs[i];
+        // ---- y = tau v^T A[r:r+L, c] (left columns), w = tau D v, z = tau E v: 4 threads per item
+        const int item = tid >> 2, part = tid & 3;
+        double sy = 0.0, sw = 0.0, sz = 0.0;   // shuffles below run on all lanes (full mask)
+        if (item >= 1 && item < nl) {
+          const int sl = sl_left(item), d0 = nl - item;   // row r sits at offset r - c
+#pragma unroll 4
+          for (int i = part; i < L; i += 4) sy += vs[i] * W[sl * LDW + d0 + i];
         }
-        // ---- (c1) w = tau D v (D skew, lower stored) and (d1) z = tau E v: 4 threads per row
-        {
-          const int row = tid >> 2, part = tid & 3;
-          double sw = 0.0, sz = 0.0;   // shuffles below run on all lanes (full mask)
-          if (row < L) {
-            for (int j = part; j < row; j += 4) sw += W[(dc + j) * LDW + (row - j)] * vs[j];
-            for (int j = row + 1 + part; j < L; j += 4) sw -= W[(dc + row) * LDW + (j - row)] * vs[j];
-          }
-          if (row < ne) {
-            for (int j = part; j < L; j += 4) sz += W[(dc + j) * LDW + (L + row - j)] * vs[j];
-          }
-          sw += __shfl_xor_sync(0xffffffffu, sw, 1);
-          sw += __shfl_xor_sync(0xffffffffu, sw, 2);
-          sz += __shfl_xor_sync(0xffffffffu, sz, 1);
-          sz += __shfl_xor_sync(0xffffffffu, sz, 2);
-          if (part == 0 && row < L) ws[row] = tau * sw;
-          if (part == 0 && row < ne) zs[row] = tau * sz;
+        if (item < L) {
+          for (int j = part; j < item; j += 4) sw += W[sl_diag(j) * LDW + (item - j)] * vs[j];
+          const int sr = sl_diag(item);
+          for (int j = item + 1 + part; j < L; j += 4) sw -= W[sr * LDW + (j - item)] * vs[j];
+        }
+        if (item < ne) {
+#pragma unroll 4
+          for (int j = part; j < L; j += 4) sz += W[sl_diag(j) * LDW + (L + item - j)] * vs[j];
+        }
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+          sy += __shfl_xor_sync(0xffffffffu, sy, o);
+          sw += __shfl_xor_sync(0xffffffffu, sw, o);
+          sz += __shfl_xor_sync(0xffffffffu, sz, o);
+        }
+        if (part == 0) {
+          if (item < nl) ys[item] = tau * sy;
+          if (item < L) ws[item] = tau * sw;
+          if (item < ne) zs[item] = tau * sz;
         }
         __syncthreads();
-        // ---- (c2) D_ij += v_i w_j - w_i v_j (i > j);  (d2) E_ij -= z_i v_j
+        CH_TS(2);
+        // ---- left block -= v y^T;  D_ij += v_i w_j - w_i v_j (i > j);  E_ij -= z_i v_j
+#pragma unroll 4
+        for (int cc = 1 + warp; cc < nl; cc += 8) {
+          const int sl = sl_left(cc), d0 = nl - cc;
+          const double yc = ys[cc];
+          for (int i = lane; i < L; i += 32) W[sl * LDW + d0 + i] -= yc * vs[i];
+        }
+#pragma unroll 4
         for (int j = warp; j < L; j += 8) {
+          const int sj = sl_diag(j);
           const double vj = vs[j], wj = ws[j];
-          for (int i = j + 1 + lane; i < L; i += 32) W[(dc + j) * LDW + (i - j)] += vs[i] * wj - ws[i] * vj;
-          for (int i = lane; i < ne; i += 32) W[(dc + j) * LDW + (L + i - j)] -= zs[i] * vj;
+          for (int i = j + 1 + lane; i < L; i += 32) W[sj * LDW + (i - j)] += vs[i] * wj - ws[i] * vj;
+          for (int i = lane; i < ne; i += 32) W[sj * LDW + (L + i - j)] -= zs[i] * vj;
         }
       }
       __syncthreads();
-      // ---- write back the touched entries
-      for (int cc = warp; cc < ncol; cc += 8) {
-        int64_t lo, hi;
-        seg(cc, lo, hi);
+      CH_TS(3);
+      // ---- write back the final entries: the left block (rows [r, r+L) of columns [col, r)),
+      //      the diagonal block, and -- on the sweep's last task -- the block below.
+      for (int cc = warp; cc < nl; cc += 8) {
         const int64_t c = col + cc;
-        for (int64_t i = lo + lane; i < hi; i += 32) __stcg(&a.AB[(i - c) + c * a.ldab], W[cc * LDW + (int)(i - c)]);
+        const int sl = sl_left(cc);
+        double* gp = a.AB + c * a.ldab + (r - c);
+        const double* wp = W + sl * LDW + (int)(r - c);
+        for (int i = lane; i < L; i += 32) __stcg(&gp[i], wp[i]);
       }
-      __threadfence();
+      for (int j = warp; j < L; j += 8) {
+        const int64_t c = r + j;
+        const int sj = sl_diag(j);
+        const int len = (int)((last ? e : r + L) - c);
+        double* gp = a.AB + c * a.ldab;
+        const double* wp = W + sj * LDW;
+        for (int i = lane; i < len; i += 32) __stcg(&gp[i], wp[i]);
+      }
       __syncthreads();
-      if (tid == 0) {
+      if (tid == 0) {   // barrier, then one GPU-scope fence + flag (the grid-barrier pattern)
+        __threadfence();
         volatile int* pr = a.progress + s;
         *pr = (int)(t + 1);
       }
+      CH_TS(4);
+      if (prof) t_work += clock64() - tk;
     }
   }
+  if (prof) { a.dbg[0] = t_wait; a.dbg[1] = t_work; a.dbg[2] = ntasks; for (int i = 0; i < 5; i++) a.dbg[3 + i] = tph[i]; }
+#undef CH_TS
 }
 
 // extract Lemma-1 alpha_k = -T[k+1, k] from the final band
@@ -880,13 +905,27 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
       ChaseArgs a;
       a.AB = w.AB; a.ldab = L.ldab; a.n = n; a.b = L.b; a.k2 = L.k2; a.progress = w.progress;
       a.qv = w.qv; a.qtau = w.qtau; a.gofs = w.gofs;
+      a.dbg = nullptr;
+      if (getenv("SKEWEIG_CHASE_DBG")) {   // debug instrumentation only
+        cudaError_t me = cudaMalloc(&a.dbg, 8 * sizeof(long long));
+        if (me) { fprintf(stderr, "[chase dbg] cudaMalloc failed: %s\n", cudaGetErrorString(me)); a.dbg = nullptr; }
+      }
       int G = chase_grid(n, L.b, nsm);
-      size_t smem = (size_t)2 * L.b * (2 * L.b + 2) * sizeof(double);
+      size_t smem = (size_t)(2 * L.b + 1) * (2 * L.b + 2) * sizeof(double);
       e = cudaFuncSetAttribute(chase_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e) return e;
       void* args[] = {&a};
       e = cudaLaunchCooperativeKernel((void*)chase_kernel<128>, dim3(G), dim3(256), args, smem, st);
       if (e) return e;
+      if (a.dbg) {
+        long long h[8];
+        cudaMemcpyAsync(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[chase dbg] G=%d tasks(cta0)=%lld  per task: wait %.0f work %.0f (load %.0f house %.0f "
+                "w/z %.0f rank2 %.0f store %.0f) cycles\n", G, h[2], (double)h[0] / h[2], (double)h[1] / h[2],
+                (double)h[3] / h[2], (double)h[4] / h[2], (double)h[5] / h[2], (double)h[6] / h[2], (double)h[7] / h[2]);
+        cudaFree(a.dbg);
+      }
     }
     alpha_from_band_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.AB, L.ldab, n, alpha);
   }
