@@ -71,6 +71,18 @@ typedef struct skew_ctx_s* skew_ctx;
 int skew_ctx_create(skew_ctx* out, int device, void* cuda_stream);
 int skew_ctx_destroy(skew_ctx ctx);
 
+/* Multi-GPU (one process per GPU).  skew_get_unique_id fills 128 bytes (an NCCL unique
+ * id) on one rank; the caller distributes them (e.g. torch.distributed) and every rank
+ * calls skew_ctx_create_dist with the same bytes.  On such a context the solve entry
+ * points are collective: every rank passes the SAME A; the full->band reduction is
+ * distributed by b-wide column blocks (1D block-cyclic, owner of column c = (c/64) mod
+ * nranks; NCCL broadcast of each panel's V, T, tau and allreduce of the skew-SYMM
+ * products); the band is combined with an allreduce; the eigenvectors
+ * are sharded by skew_eig_range (each rank its own [k0, k1)).  Requires SKEWEIG_B = 64.
+ * Returns SKEW_ERR_NCCL on communicator failure. */
+int skew_get_unique_id(char id[128]);
+int skew_ctx_create_dist(skew_ctx* out, int device, void* cuda_stream, int nranks, int rank, const char id[128]);
+
 /* Bytes of device workspace a solve of order n with nev pairs needs (flags:
  * SKEW_WS_*).  The caller allocates it (e.g. a torch uint8 tensor) and passes it
  * with skew_set_workspace; it must stay alive while the context uses it. */

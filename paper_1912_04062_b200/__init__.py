@@ -36,6 +36,9 @@ _dp = ctypes.c_void_p
 EXPORTS = {
     "skew_ctx_create": ([ctypes.POINTER(_vp), ctypes.c_int, _vp], ctypes.c_int),
     "skew_ctx_destroy": ([_vp], ctypes.c_int),
+    "skew_get_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+    "skew_ctx_create_dist": ([ctypes.POINTER(_vp), ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p],
+                             ctypes.c_int),
     "skew_workspace_size": ([_vp, _i64, _i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "skew_set_workspace": ([_vp, _vp, ctypes.c_size_t], ctypes.c_int),
     "skew_eig": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
@@ -90,16 +93,35 @@ def _torch():
 class Context:
     """One C-ABI context per (device, stream) plus a torch-allocated device workspace."""
 
-    def __init__(self, device=None, stream=None):
+    def __init__(self, device=None, stream=None, group=None, distributed=False):
+        """distributed=True: a collective context over torch.distributed `group` (NCCL inside the
+        library; the unique id is exchanged with broadcast_object_list)."""
         torch = _torch()
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    torch.device(device).index or 0)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         h = _vp()
-        rc = lib().skew_ctx_create(ctypes.byref(h), self.device.index, _vp(self.stream.cuda_stream))
+        if distributed:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            buf = ctypes.create_string_buffer(128)
+            if rank == 0:
+                rc = lib().skew_get_unique_id(buf)
+                if rc != 0:
+                    raise SkewError(rc, "skew_get_unique_id failed")
+            obj = [bytes(buf.raw) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            idb = ctypes.create_string_buffer(obj[0], 128)
+            rc = lib().skew_ctx_create_dist(ctypes.byref(h), self.device.index, _vp(self.stream.cuda_stream), world,
+                                            rank, idb)
+            self.rank, self.world = rank, world
+        else:
+            rc = lib().skew_ctx_create(ctypes.byref(h), self.device.index, _vp(self.stream.cuda_stream))
+            self.rank, self.world = 0, 1
         if rc != 0:
-            raise SkewError(rc, "skew_ctx_create failed")
+            raise SkewError(rc, "skew context creation failed")
         self.h = h
         self.ws = None
 

@@ -24,12 +24,12 @@ HEADERS = ["common.cuh", "gemm_dmma.cuh", "internal.h"]
 def _nccl_flags():
     """NCCL: torch's bundled libnccl (2.28) if present, else the system one."""
     try:
-        import nvidia.nccl as nn  # noqa
-        d = os.path.dirname(nn.__file__)
+        import nvidia.nccl as nn  # noqa  (namespace package: no __file__)
+        d = list(nn.__path__)[0]
         inc = os.path.join(d, "include")
         lib = os.path.join(d, "lib")
         if os.path.exists(os.path.join(inc, "nccl.h")):
-            return ["-I" + inc], ["-L" + lib, "-Wl,-rpath," + lib, "-l:libnccl.so.2"]
+            return ["-I" + inc], ["-L" + lib, "-Xlinker", "-rpath=" + lib, "-l:libnccl.so.2"]
     except Exception:
         pass
     return [], ["-lnccl"]

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <string>
 #include <algorithm>
+#include <nccl.h>
 
 namespace sk {
 
@@ -54,7 +55,7 @@ static void plan_layout(Ctx& c, Plan& p, Arena& ar, int64_t n, int64_t nev, int 
   if (vec) {
     p.Q = ar.take<double>((size_t)p.ldn * std::max<int64_t>(nev, 1));
     p.X = ar.take<double>((size_t)p.ldn * 2 * std::max<int64_t>(nev, 1));
-    bt1_reserve(ar, n, 2 * nev, c.prm.bt1_merge * b, p.b1);
+    bt1_reserve(ar, p.f2b, 2 * nev, p.b1);
   }
   p.status = ar.take<int64_t>(4);
   p.scratch = ar.take<double>(64);
@@ -159,8 +160,41 @@ int skew_ctx_create(skew_ctx* out, int device, void* cuda_stream) {
   return SKEW_OK;
 }
 
+int skew_get_unique_id(char id[128]) {
+  if (!id) return -1;
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return SKEW_ERR_NCCL;
+  static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id, &u, 128);
+  return SKEW_OK;
+}
+
+int skew_ctx_create_dist(skew_ctx* out, int device, void* cuda_stream, int nranks, int rank, const char id[128]) {
+  if (!out) return -1;
+  if (nranks < 1) return -4;
+  if (rank < 0 || rank >= nranks) return -5;
+  if (!id) return -6;
+  int rc = skew_ctx_create(out, device, cuda_stream);
+  if (rc != SKEW_OK) return rc;
+  skew_ctx ctx = *out;
+  ctx->c.nranks = nranks;
+  ctx->c.rank = rank;
+  if (nranks > 1) {
+    if (ctx->c.prm.b != 64) { skew_ctx_destroy(ctx); *out = nullptr; return SKEW_ERR_NOT_IMPLEMENTED; }
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclComm_t comm;
+    ncclResult_t r = ncclCommInitRank(&comm, nranks, u, rank);
+    if (r != ncclSuccess) { skew_ctx_destroy(ctx); *out = nullptr; return SKEW_ERR_NCCL; }
+    ctx->c.nccl = comm;
+  }
+  return SKEW_OK;
+}
+
 int skew_ctx_destroy(skew_ctx ctx) {
   if (!ctx) return -1;
+  if (ctx->c.nccl) ncclCommDestroy((ncclComm_t)ctx->c.nccl);
   for (int s = 0; s < ST_COUNT; s++) { cudaEventDestroy(ctx->ev_start[s]); cudaEventDestroy(ctx->ev_stop[s]); }
   delete ctx;
   return SKEW_OK;
@@ -241,16 +275,23 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   const bool vec = (Zre != nullptr);
   // ---- full -> band
   tstart(ctx, ST_F2B);
+  Dist d;
+  d.P = c.nranks; d.rank = c.rank; d.comm = c.nccl;
   if (p.f2b.npanel > 0) {
     CK(cudaMemsetAsync(p.vstore, 0, sizeof(double) * p.f2b.vstore_elems, st), "memset vstore");
-    CK(f2b_run(p.f2b, A_d, lda, p.vstore, p.fw, c.num_sms, st), "f2b");
+    int nerr = 0;
+    cudaError_t fe = f2b_run(p.f2b, A_d, lda, p.vstore, p.fw, c.num_sms, st, d, &nerr);
+    if (nerr) { c.last_error = std::string("f2b: NCCL ") + ncclGetErrorString((ncclResult_t)nerr); return SKEW_ERR_NCCL; }
+    CK(fe, "f2b");
   }
   tstop(ctx, ST_F2B);
   // ---- band -> tridiagonal
   tstart(ctx, ST_B2T);
-  const int bw = (int)std::min<int64_t>(c.prm.b, std::max<int64_t>(n - 1, 1));
-  (void)bw;
-  CK(band_extract(A_d, lda, n, c.prm.b, p.bw.AB, p.b2t.ldab, st), "band extract");
+  CK(band_extract(A_d, lda, n, c.prm.b, p.bw.AB, p.b2t.ldab, st, d.P, d.rank), "band extract");
+  if (d.P > 1) {   // every rank contributed the band columns it owns
+    ncclResult_t r = ncclAllReduce(p.bw.AB, p.bw.AB, (size_t)p.b2t.ldab * n, ncclDouble, ncclSum, (ncclComm_t)d.comm, st);
+    if (r != ncclSuccess) { c.last_error = std::string("band allreduce: NCCL ") + ncclGetErrorString(r); return SKEW_ERR_NCCL; }
+  }
   CK(b2t_run(p.b2t, p.bw, p.alpha, c.num_sms, st), "b2t");
   tstop(ctx, ST_B2T);
   // ---- tridiagonal eigenproblem
@@ -271,7 +312,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
     CK(bt2_run(p.b2t, p.bw, p.X, p.ldn, 2 * nloc, st), "bt2");
     tstop(ctx, ST_BT2);
     tstart(ctx, ST_BT1);
-    if (p.f2b.npanel > 0) CK(bt1_run(p.f2b, p.vstore, p.fw.tau, p.X, p.ldn, 2 * nloc, p.b1, st), "bt1");
+    if (p.f2b.npanel > 0) CK(bt1_run(p.f2b, p.vstore, p.fw.tau, p.fw.T, p.X, p.ldn, 2 * nloc, p.b1, st), "bt1");
     tstop(ctx, ST_BT1);
   }
   // ---- output
@@ -418,7 +459,9 @@ int skew_stage_reduce_to_band(skew_ctx ctx, int64_t n, double* A, int64_t lda, d
   tstart(ctx, ST_F2B);
   if (p.f2b.npanel > 0) {
     CK(cudaMemsetAsync(p.vstore, 0, sizeof(double) * p.f2b.vstore_elems, st), "memset");
-    CK(f2b_run(p.f2b, A, lda, p.vstore, p.fw, ctx->c.num_sms, st), "f2b");
+    Dist d1;   // stage entry: single device
+    int nerr = 0;
+    CK(f2b_run(p.f2b, A, lda, p.vstore, p.fw, ctx->c.num_sms, st, d1, &nerr), "f2b");
   }
   tstop(ctx, ST_F2B);
   const int b = p.f2b.b;

@@ -224,12 +224,15 @@ __global__ void alpha_from_band_kernel(const double* AB, int64_t ldab, int64_t n
   if (k < n - 1) alpha[k] = -AB[1 + k * ldab];
 }
 
-// band from the F2B output A (A[c+d, c], d <= b) into AB (ldab rows, zero beyond b)
-__global__ void band_extract_kernel(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab) {
+// band from the F2B output A (A[c+d, c], d <= b) into AB (ldab rows, zero beyond b).
+// Distributed: only the rank owning column c ((c / b) mod P) contributes its column.
+__global__ void band_extract_kernel(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, int P,
+                                    int rank) {
   int64_t c = blockIdx.x;
+  const bool mine = ((c / b) % P) == rank;
   for (int d = threadIdx.x; d < ldab; d += blockDim.x) {
     double v = 0.0;
-    if (d >= 1 && d <= b && c + d < n) v = A[SK_IDX(c + d, c, lda)];
+    if (mine && d >= 1 && d <= b && c + d < n) v = A[SK_IDX(c + d, c, lda)];
     AB[d + c * ldab] = v;
   }
 }
@@ -858,9 +861,10 @@ void B2TLayout::init(int64_t n_, int b_, int k2_) {
   ngroups = g;
 }
 
-cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st) {
+cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st,
+                         int P, int rank) {
   KScope ks(KC_BAND, st);
-  band_extract_kernel<<<(unsigned)std::max<int64_t>(n, 1), 128, 0, st>>>(A, lda, n, b, AB, ldab);
+  band_extract_kernel<<<(unsigned)std::max<int64_t>(n, 1), 128, 0, st>>>(A, lda, n, b, AB, ldab, P, rank);
   return cudaGetLastError();
 }
 cudaError_t band_copy(const double* ABin, int64_t ldin, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st) {

@@ -13,62 +13,133 @@
 #include "gemm_dmma.cuh"
 #include "internal.h"
 #include <algorithm>
+#include <vector>
 
 namespace sk {
 
-// T_g (K x K upper) from the Gram G (K x K, full) and tau (K): thread per row
-__global__ void bt1_tbuild_kernel(const double* G, int K, const double* tau, double* T) {
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= K) return;
-  // row r of T: T[r][r] = tau_r; T[r][c] = -tau_c * sum_{l=r}^{c-1} T[r][l] G[l][c]
-  // (stored directly into T to avoid a large local array)
-  for (int c = 0; c < K; c++) T[r + (size_t)c * K] = 0.0;
-  T[r + (size_t)r * K] = tau[r];
-  for (int c = r + 1; c < K; c++) {
-    double s = 0.0;
-    for (int l = r; l < c; l++) s += T[r + (size_t)l * K] * G[l + (size_t)c * K];
-    T[r + (size_t)c * K] = -tau[c] * s;
+// ---- merged-group preparation, all groups at once (before the BT1 loop) ----------------
+// Gram G_g = V_g^T V_g (K x K) for every group: grid (K/64, K/64, ngroup) of DMMA tiles.
+__global__ void __launch_bounds__(128) bt1_gram_kernel(const double* vstore, const int64_t* gmeta, int K,
+                                                       double* G) {
+  using T = GemmTile<64, 64, 16, 32, 32, 2, true, false>;
+  extern __shared__ __align__(16) double smem[];
+  const int64_t g = blockIdx.z;
+  const int64_t goff = gmeta[3 * g], ld = gmeta[3 * g + 1], m = gmeta[3 * g + 2];
+  const double* V = vstore + goff;
+  GemmArgs ga;
+  ga.M = K; ga.N = K; ga.K = m;
+  ga.A = V; ga.lda = ld; ga.B = V; ga.ldb = ld;
+  ga.vec = gemm_vec_ok(V, ld, V, ld) ? 1 : 0;
+  double acc[T::FM][T::FN][2];
+#pragma unroll
+  for (int i = 0; i < T::FM; i++)
+#pragma unroll
+    for (int j = 0; j < T::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int64_t m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  T::mainloop(ga, smem, m0, n0, 0, m, acc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm0 = (warp % T::NWARP_M) * 32, wn0 = (warp / T::NWARP_M) * 32;
+  const int gq = lane >> 2, t = lane & 3;
+  double* out = G + (size_t)g * K * K;
+#pragma unroll
+  for (int i = 0; i < T::FM; i++)
+#pragma unroll
+    for (int j = 0; j < T::FN; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        out[(m0 + wm0 + 8 * i + gq) + (n0 + wn0 + 8 * j + 2 * t + h) * (size_t)K] = acc[i][j][h];
+}
+
+// Merged T_g (K x K upper, K = merge*b) from the per-panel T_q (b x b, from the full->band
+// reduction) and the Gram: block column q of the forward recurrence is
+//   T[0:qb, q] = -T[0:qb, 0:qb] (V_{0:q}^T V_q) T_q,   T[q, q] = T_q
+// (Schreiber-Van Loan).  One CTA per group; operands through L1/L2.
+__global__ void __launch_bounds__(256) bt1_tmerge_kernel(const double* G, const double* Tpanel, int64_t npanel,
+                                                         int merge, int b, double* Tm, double* Y) {
+  const int64_t g = blockIdx.x;
+  const int K = merge * b;
+  const double* Gg = G + (size_t)g * K * K;
+  double* T = Tm + (size_t)g * K * K;
+  double* Yg = Y + (size_t)g * K * b;
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    const int r = e % K, c = e / K, qr = r / b, qc = c / b;
+    const int64_t j = g * merge + qc;
+    T[e] = (qr == qc && j < npanel) ? Tpanel[(size_t)j * b * b + (r % b) + (size_t)(c % b) * b] : 0.0;
+  }
+  __syncthreads();
+  for (int q = 1; q < merge; q++) {
+    const int64_t j = g * merge + q;
+    if (j >= npanel) break;
+    const int R = q * b;
+    const double* Tq = Tpanel + (size_t)j * b * b;
+    // Y = G[0:R, qb:(q+1)b] T_q   (R x b)
+    for (int e = threadIdx.x; e < R * b; e += blockDim.x) {
+      const int r = e % R, c = e / R;
+      double s = 0.0;
+      for (int l = 0; l <= c; l++) s += Gg[r + (size_t)(q * b + l) * K] * Tq[l + (size_t)c * b];
+      Yg[e] = s;
+    }
+    __syncthreads();
+    // T[0:R, qb+c] = -T[0:R, 0:R] Y[:, c]   (T upper: l >= r)
+    for (int e = threadIdx.x; e < R * b; e += blockDim.x) {
+      const int r = e % R, c = e / R;
+      double s = 0.0;
+      for (int l = r; l < R; l++) s += T[r + (size_t)l * K] * Yg[l + (size_t)c * R];
+      T[r + (size_t)(q * b + c) * K] = -s;
+    }
+    __syncthreads();
   }
 }
 
-
-void bt1_reserve(Arena& ar, int64_t n, int64_t ncols, int K, BT1Work& w) {
+void bt1_reserve(Arena& ar, const F2BLayout& L, int64_t ncols, BT1Work& w) {
+  const int64_t n = L.n;
+  const int K = L.merge * L.b;
+  const int64_t ng = std::max<int64_t>(L.ngroup, 1);
   int64_t ldn = (std::max<int64_t>(n, 2) + 1) & ~int64_t(1);
-  w.G = ar.take<double>((size_t)K * K);
-  w.T = ar.take<double>((size_t)K * K);
+  w.G = ar.take<double>((size_t)ng * K * K);
+  w.T = ar.take<double>((size_t)ng * K * K);
+  w.Y = ar.take<double>((size_t)ng * K * L.b);
   w.U = ar.take<double>((size_t)ldn * K);
   w.Z = ar.take<double>((size_t)K * std::max<int64_t>(ncols, 1));
+  w.gmeta = ar.take<int64_t>((size_t)3 * ng);
 }
 
-cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, double* X, int64_t ldx,
-                    int64_t ncols, BT1Work& w, cudaStream_t st) {
+cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,
+                    int64_t ldx, int64_t ncols, BT1Work& w, cudaStream_t st) {
+  (void)tau_all;
   cudaError_t e;
   const int b = L.b;
+  const int K = L.merge * b;
+  if (L.ngroup == 0) return cudaSuccess;
+  {   // all groups: Gram and merged T
+    std::vector<int64_t> meta(3 * L.ngroup);
+    for (int64_t g = 0; g < L.ngroup; g++) {
+      meta[3 * g] = L.goff[g];
+      meta[3 * g + 1] = L.gld[g];
+      meta[3 * g + 2] = L.n - L.r0(g * L.merge);
+    }
+    e = cudaMemcpyAsync(w.gmeta, meta.data(), sizeof(int64_t) * meta.size(), cudaMemcpyHostToDevice, st);
+    if (e) return e;
+    e = cudaStreamSynchronize(st);   // `meta` is a host temporary
+    if (e) return e;
+    KScope ks(KC_BT1_PREP, st, 2);
+    using TG = GemmTile<64, 64, 16, 32, 32, 2, true, false>;
+    bt1_gram_kernel<<<dim3(K / 64, K / 64, (unsigned)L.ngroup), 128, TG::SMEM_BYTES, st>>>(vstore, w.gmeta, K, w.G);
+    bt1_tmerge_kernel<<<(unsigned)L.ngroup, 256, 0, st>>>(w.G, Tpanel, L.npanel, L.merge, b, w.T, w.Y);
+  }
   for (int64_t g = L.ngroup - 1; g >= 0; g--) {
-    const int64_t j0 = g * L.merge;
-    const int64_t j1 = std::min<int64_t>(L.npanel, j0 + L.merge);
-    const int K = (int)((j1 - j0) * b);
-    const int64_t r0 = L.r0(j0);
+    const int64_t r0 = L.r0(g * L.merge);
     const int64_t m = L.n - r0;
     const double* V = vstore + L.goff[g];
     const int64_t ldv = L.gld[g];
-    // Gram G = V^T V
-    {
-      KScope ks(KC_BT1_PREP, st, 3);
-      GemmArgs ga;
-      ga.M = K; ga.N = K; ga.K = m;
-      ga.A = V; ga.lda = ldv; ga.B = V; ga.ldb = ldv; ga.C = w.G; ga.ldc = K; ga.alpha = 1.0; ga.beta = 0.0;
-      e = gemm_dmma<64, 64, 16, 32, 16, 4, true, false, false>(ga, st);
-      if (e) return e;
-      bt1_tbuild_kernel<<<(K + 63) / 64, 64, 0, st>>>(w.G, K, tau_all + j0 * b, w.T);
-    }
+    const double* Tg = w.T + (size_t)g * K * K;
     // U = V T^T
     const int64_t ldu = (m + 1) & ~int64_t(1);
     {
-      KScope ks(KC_BT1_PREP, st, 0);
+      KScope ks(KC_BT1_PREP, st, 1);
       GemmArgs ga;
       ga.M = m; ga.N = K; ga.K = K;
-      ga.A = V; ga.lda = ldv; ga.B = w.T; ga.ldb = K; ga.C = w.U; ga.ldc = ldu; ga.alpha = 1.0; ga.beta = 0.0;
+      ga.A = V; ga.lda = ldv; ga.B = Tg; ga.ldb = K; ga.C = w.U; ga.ldc = ldu; ga.alpha = 1.0; ga.beta = 0.0;
       e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, false>(ga, st);
       if (e) return e;
     }

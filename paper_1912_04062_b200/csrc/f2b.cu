@@ -15,6 +15,7 @@
 #include "internal.h"
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <nccl.h>
 
 namespace cg = cooperative_groups;
 
@@ -272,6 +273,7 @@ struct SymmArgs {
   double* X; int64_t ldx;
   int64_t m; int nb;
   int vec;
+  int P = 1, qoff = 0;   // distributed: only column blocks q = qoff (mod P) of S are local
 };
 
 template <int BM, int NB, int BK, int STAGES>
@@ -290,23 +292,26 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
 #pragma unroll
     for (int j = 0; j < TR::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // ---------------- row part: K in [0, min(m, (p+1)BM))
+  // ---------------- row part: K over the local column blocks q <= p (q = qoff mod P)
   {
     GemmArgs g;
     g.M = s.m; g.N = s.nb; g.K = smin<int64_t>(s.m, m0 + BM);
     g.A = s.S; g.lda = s.lds; g.B = s.U; g.ldb = s.ldu; g.vec = s.vec;
     double* As = smem;
     double* Bs = smem + STAGES * TR::A_STAGE;
-    const int64_t nk = (g.K + BK - 1) / BK;
+    constexpr int KPB = BM / BK;   // k-steps per column block
+    const int64_t nq = (p >= s.qoff) ? (p - s.qoff) / s.P + 1 : 0;
+    const int64_t nk = nq * KPB;
+    auto kofs = [&](int64_t kb) -> int64_t { return (s.qoff + s.P * (kb / KPB)) * (int64_t)BM + (kb % KPB) * BK; };
     for (int st = 0; st < STAGES - 1; st++) {
-      if (st < nk) TR::load_stage(g, As + st * TR::A_STAGE, Bs + st * TR::B_STAGE, m0, 0, st * BK, tid);
+      if (st < nk) TR::load_stage(g, As + st * TR::A_STAGE, Bs + st * TR::B_STAGE, m0, 0, kofs(st), tid);
       cp_async_commit();
     }
     for (int64_t kb = 0; kb < nk; kb++) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
       const int cs = (int)(kb % STAGES);
-      const int64_t k0 = kb * BK;
+      const int64_t k0 = kofs(kb);
       if (k0 + BK > m0) {   // diagonal tile: keep row > col only
         double* a = As + cs * TR::A_STAGE;
         for (int e = tid; e < BK * BM; e += NT) {
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
       int64_t pf = kb + STAGES - 1;
       if (pf < nk) {
         int ps = (int)(pf % STAGES);
-        TR::load_stage(g, As + ps * TR::A_STAGE, Bs + ps * TR::B_STAGE, m0, 0, pf * BK, tid);
+        TR::load_stage(g, As + ps * TR::A_STAGE, Bs + ps * TR::B_STAGE, m0, 0, kofs(pf), tid);
       }
       cp_async_commit();
       TR::mma_stage(As + cs * TR::A_STAGE, Bs + cs * TR::B_STAGE, acc, wm0, wn0, lane);
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
     g.A = s.S; g.lda = s.lds; g.B = s.U; g.ldb = s.ldu; g.vec = s.vec;
     double* As = smem;
     double* Bs = smem + STAGES * TC::A_STAGE;
-    const int64_t nk = (s.m - m0 + BK - 1) / BK;
+    const int64_t nk = (((p - s.qoff) % s.P + s.P) % s.P == 0) ? (s.m - m0 + BK - 1) / BK : 0;   // local column p
     for (int st = 0; st < STAGES - 1; st++) {
       if (st < nk) TC::load_stage(g, As + st * TC::A_STAGE, Bs + st * TC::B_STAGE, m0, 0, m0 + st * BK, tid);
       cp_async_commit();
@@ -509,7 +514,9 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
 }
 
 cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, double* vstore, const F2BWork& w,
-                       cudaStream_t st) {
+                       cudaStream_t st, const Dist& d, int* nccl_err) {
+  // distributed: trailing column block q (global block j+1+q) is local iff (j+1+q) mod P == rank
+  const int qoff = (int)((((int64_t)d.rank - (j + 1)) % d.P + d.P) % d.P);
   const int b = L.b;
   const int64_t r0 = L.r0(j), m = L.n - r0;
   const int64_t g = j / L.merge, pl = j % L.merge;
@@ -532,6 +539,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     SymmArgs s;
     s.S = S; s.lds = lda; s.U = w.U; s.ldu = ldn; s.X = Wp; s.ldx = ldn; s.m = m; s.nb = b;
     s.vec = gemm_vec_ok(S, lda, w.U, ldn) ? 1 : 0;
+    s.P = d.P; s.qoff = qoff;
     using TR = GemmTile<kSymmBM, 64, kSymmBK, 32, 32, kSymmStages, false, false>;
     using TC = GemmTile<kSymmBM, 64, kSymmBK, 32, 32, kSymmStages, true, false>;
     size_t smem = std::max(TR::SMEM_BYTES, TC::SMEM_BYTES);
@@ -544,6 +552,10 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     }
     KScope ks(KC_SYMM, st);
     symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)((m + kSymmBM - 1) / kSymmBM), TR::NTHREADS, smem, st>>>(s);
+  }
+  if (d.P > 1) {   // Y = sum over ranks of the partial skew-SYMM products (NVLink allreduce)
+    ncclResult_t r = ncclAllReduce(Wp, Wp, (size_t)ldn * b, ncclDouble, ncclSum, (ncclComm_t)d.comm, st);
+    if (r != ncclSuccess) { *nccl_err = (int)r; return cudaErrorUnknown; }
   }
   {   // W = X - 1/2 V (T^T (V^T X));  P = [V W], Q = [W -V]
     KScope ks(KC_WCORR, st, 5);
@@ -565,6 +577,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
   GemmArgs ga;
   ga.M = m; ga.N = m; ga.K = 2 * b;
   ga.A = w.P; ga.lda = ldn; ga.B = w.Q; ga.ldb = ldn; ga.C = S; ga.ldc = lda; ga.alpha = 1.0; ga.beta = 1.0;
+  ga.col_stride = d.P; ga.col_off = qoff;   // update only the local column blocks
   {
     KScope ks(KC_R2K, st);
     e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
@@ -575,13 +588,33 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
 
 // Whole F2B: A (n x n, lda, strictly lower) -> band of width b in A[c+1..c+b, c],
 // reflectors in vstore (layout L), tau / T per panel in w.
+// Distributed (d.P > 1, b = 64): panel j is factored by its owner (j mod P) and broadcast
+// (V_j, T_j, tau_j); every rank forms its partial skew-SYMM from its local column blocks,
+// the partial products are summed with an allreduce, W is formed redundantly and each rank
+// updates only its local column blocks.
 cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, const F2BWork& w, int nsm,
-                    cudaStream_t st) {
+                    cudaStream_t st, const Dist& d, int* nccl_err) {
   cudaError_t e;
+  if (d.P > 1 && L.b != 64) return cudaErrorInvalidValue;
   for (int64_t j = 0; j < L.npanel; j++) {
-    e = f2b_panel(L, j, A, lda, vstore, w, nsm, st);
-    if (e) return e;
-    e = f2b_update(L, j, A, lda, vstore, w, st);
+    const int owner = (int)(j % d.P);
+    if (d.rank == owner) {
+      e = f2b_panel(L, j, A, lda, vstore, w, nsm, st);
+      if (e) return e;
+    }
+    if (d.P > 1) {
+      const int64_t g = j / L.merge, pl = j % L.merge;
+      double* Vcols = vstore + L.goff[g] + pl * (int64_t)L.b * L.gld[g];   // the panel's columns of the group block
+      ncclComm_t comm = (ncclComm_t)d.comm;
+      ncclResult_t r = ncclGroupStart();
+      if (r == ncclSuccess) r = ncclBroadcast(Vcols, Vcols, (size_t)L.gld[g] * L.b, ncclDouble, owner, comm, st);
+      if (r == ncclSuccess) r = ncclBroadcast(w.T + j * (int64_t)L.b * L.b, w.T + j * (int64_t)L.b * L.b,
+                                              (size_t)L.b * L.b, ncclDouble, owner, comm, st);
+      if (r == ncclSuccess) r = ncclBroadcast(w.tau + j * L.b, w.tau + j * L.b, (size_t)L.b, ncclDouble, owner, comm, st);
+      ncclResult_t r2 = ncclGroupEnd();
+      if (r != ncclSuccess || r2 != ncclSuccess) { *nccl_err = (int)(r != ncclSuccess ? r : r2); return cudaErrorUnknown; }
+    }
+    e = f2b_update(L, j, A, lda, vstore, w, st, d, nccl_err);
     if (e) return e;
   }
   return cudaSuccess;

@@ -28,6 +28,8 @@ struct GemmArgs {
   double alpha, beta;
   int64_t tri_off = 1;   // TRI: write element (m, n) iff m - n >= tri_off (1: strictly lower, 0: incl. diagonal)
   int vec = 1;           // 1: 16-byte cp.async (A, B 16B-aligned, lda/ldb even); 0: 8-byte copies
+  int col_stride = 1;    // TRI with BM == BN: only column tiles tn = col_off + col_stride*i (1D block-cyclic
+  int col_off = 0;       //   column ownership of the distributed full->band reduction)
 };
 
 // true when both operands allow 16-byte (2 x double) vector copies
@@ -177,6 +179,20 @@ __device__ __forceinline__ void tri_tile(int64_t t, int R, int64_t& tm, int64_t&
   tn = t - (int64_t)R * r * (r + 1) / 2;
 }
 
+// Strided variant (BM == BN): column tiles tn_i = off + stride*i, rows tm in [tn_i, ntm);
+// S(k) = sum_{i<k} (ntm - tn_i) = k (ntm - off) - stride k (k-1) / 2.
+__device__ __forceinline__ void tri_tile_strided(int64_t t, int64_t ntm, int stride, int off, int64_t& tm,
+                                                 int64_t& tn) {
+  auto S = [&](int64_t k) -> int64_t { return k * (ntm - off) - (int64_t)stride * k * (k - 1) / 2; };
+  const double A = 0.5 * stride, B = (double)(ntm - off) + 0.5 * stride;
+  int64_t k = (int64_t)((B - sqrt(fmax(B * B - 4.0 * A * (double)t, 0.0))) / (2.0 * A));
+  if (k < 0) k = 0;
+  while (S(k + 1) <= t) k++;
+  while (k > 0 && S(k) > t) k--;
+  tn = off + (int64_t)stride * k;
+  tm = tn + (t - S(k));
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJ, bool B_NMAJ, bool TRI>
 __global__ void __launch_bounds__(GemmTile<BM, BN, BK, WM, WN, STAGES, A_KMAJ, B_NMAJ>::NTHREADS)
 gemm_dmma_kernel(GemmArgs g) {
@@ -184,7 +200,8 @@ gemm_dmma_kernel(GemmArgs g) {
   extern __shared__ __align__(16) double smem[];
   int64_t tm, tn;
   if (TRI) {
-    tri_tile(blockIdx.x, BM / BN, tm, tn);
+    if (g.col_stride > 1) tri_tile_strided(blockIdx.x, (g.M + BM - 1) / BM, g.col_stride, g.col_off, tm, tn);
+    else tri_tile(blockIdx.x, BM / BN, tm, tn);
   } else {
     tm = blockIdx.x;
     tn = blockIdx.y;
@@ -245,7 +262,13 @@ cudaError_t gemm_dmma(const GemmArgs& g, cudaStream_t st) {
   int64_t tm = (g.M + BM - 1) / BM, tn = (g.N + BN - 1) / BN;
   dim3 grid;
   static_assert(!TRI || BM % BN == 0, "TRI needs BM = R * BN");
-  if (TRI) grid = dim3((unsigned)((BM / BN) * tm * (tm + 1) / 2));
+  if (TRI && g.col_stride > 1) {
+    if (BM != BN) return cudaErrorInvalidValue;
+    const int64_t off = g.col_off, st = g.col_stride;
+    if (off >= tm) return cudaSuccess;
+    const int64_t kmax = (tm - off + st - 1) / st;
+    grid = dim3((unsigned)(kmax * (tm - off) - st * kmax * (kmax - 1) / 2));
+  } else if (TRI) grid = dim3((unsigned)((BM / BN) * tm * (tm + 1) / 2));
   else grid = dim3((unsigned)tm, (unsigned)tn);
   kern<<<grid, T::NTHREADS, T::SMEM_BYTES, st>>>(ga);
   return cudaGetLastError();

@@ -166,21 +166,31 @@ struct TridWork {
 };
 
 struct BT1Work {
-  double* G = nullptr;     // K x K
-  double* T = nullptr;     // K x K
+  double* G = nullptr;     // ngroup x K x K  Gram matrices
+  double* T = nullptr;     // ngroup x K x K  merged compact-WY T
+  double* Y = nullptr;     // ngroup x K x b  T-merge scratch
   double* U = nullptr;     // n x K
   double* Z = nullptr;     // K x ncols
+  int64_t* gmeta = nullptr;   // per group: V-store offset, ld, rows
+};
+
+// multi-GPU: 1D block-cyclic ownership of b-wide column blocks (owner of column c = (c / b) mod P)
+struct Dist {
+  int P = 1, rank = 0;
+  void* comm = nullptr;   // ncclComm_t
 };
 
 // f2b.cu
 void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w);
+// returns cudaErrorUnknown + sets *nccl_err on an NCCL failure
 cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, const F2BWork& w, int nsm,
-                    cudaStream_t st);
+                    cudaStream_t st, const Dist& d, int* nccl_err);
 // b2t.cu
 void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w);
 cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cudaStream_t st);
 cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st);
-cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st);
+cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st,
+                         int P = 1, int rank = 0);
 cudaError_t band_copy(const double* ABin, int64_t ldin, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st);
 // tridiag.cu
 void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, int window);
@@ -190,9 +200,9 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
                      int64_t* vlo_out);
 cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st);
 // bt1.cu
-void bt1_reserve(Arena& ar, int64_t n, int64_t ncols, int K, BT1Work& w);
-cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, double* X, int64_t ldx,
-                    int64_t ncols, BT1Work& w, cudaStream_t st);
+void bt1_reserve(Arena& ar, const F2BLayout& L, int64_t ncols, BT1Work& w);
+cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,
+                    int64_t ldx, int64_t ncols, BT1Work& w, cudaStream_t st);
 cudaError_t split_output(const double* X, int64_t ldx, int64_t n, int64_t nev, double* Zre, double* Zim, int64_t ldz,
                          cudaStream_t st);
 // bse.cu

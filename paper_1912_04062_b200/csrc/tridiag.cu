@@ -282,6 +282,7 @@ __global__ void td_reduce_partials(const double* part, int nchunks, int cnt, dou
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= cnt) return;
   double s = 0.0;
+#pragma unroll 8
   for (int c = 0; c < nchunks; c++) s += part[(size_t)c * cnt + e];
   out[e] = s;
 }
@@ -301,40 +302,47 @@ __global__ void td_sub_proj(const double* Qp, int64_t ldq, int p, const double* 
     Y[SK_IDX(r, j, ldy)] -= s;
   }
 }
-// Cholesky of the nb x nb Gram (in place, lower) -> R^{-1} upper in Rinv (single CTA)
+// Cholesky of the nb x nb Gram (nb <= 32) -> R^{-1} (upper) in Rinv.  One warp: column j of L
+// is finished by lane-parallel updates (right-looking), then the triangular inverse is
+// formed column by column with lane-parallel dot products.
 __global__ void td_chol_inv(const double* Gm, int nb, double* Rinv) {
-  __shared__ double L[32 * 32];
-  __shared__ double Li[32 * 32];
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) { L[e] = Gm[e]; Li[e] = 0.0; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < nb; j++) {
-      double d = L[j + j * nb];
-      for (int k = 0; k < j; k++) d -= L[j + k * nb] * L[j + k * nb];
-      d = sqrt(fmax(d, 1e-300));
-      L[j + j * nb] = d;
-      for (int i = j + 1; i < nb; i++) {
-        double s = L[i + j * nb];
-        for (int k = 0; k < j; k++) s -= L[i + k * nb] * L[j + k * nb];
-        L[i + j * nb] = s / d;
-      }
+  __shared__ double L[32][33];
+  __shared__ double Li[32][33];
+  const int lane = threadIdx.x;
+  if (lane >= 32) return;
+  for (int j = 0; j < nb; j++) {
+    for (int i = lane; i < nb; i += 32) { L[i][j] = Gm[i + j * nb]; Li[i][j] = 0.0; }
+  }
+  __syncwarp();
+  for (int j = 0; j < nb; j++) {
+    const double d = sqrt(fmax(L[j][j], 1e-300));
+    __syncwarp();
+    if (lane > j && lane < nb) L[lane][j] /= d;
+    if (lane == j) L[j][j] = d;
+    __syncwarp();
+    // trailing update: L[i][k] -= L[i][j] L[k][j] for k > j, i >= k (lane = i)
+    if (lane > j && lane < nb) {
+      const double lij = L[lane][j];
+      for (int k = j + 1; k <= lane; k++) L[lane][k] -= lij * L[k][j];
     }
-    // inverse of lower L (Li lower)
-    for (int j = 0; j < nb; j++) {
-      Li[j + j * nb] = 1.0 / L[j + j * nb];
-      for (int i = j + 1; i < nb; i++) {
-        double s = 0.0;
-        for (int k = j; k < i; k++) s += L[i + k * nb] * Li[k + j * nb];
-        Li[i + j * nb] = -s / L[i + i * nb];
-      }
+    __syncwarp();
+  }
+  // inverse of lower L: column j (lane = i): Li[i][j] = -(sum_{k=j}^{i-1} L[i][k] Li[k][j]) / L[i][i]
+  for (int j = 0; j < nb; j++) {
+    if (lane == j) Li[j][j] = 1.0 / L[j][j];
+    __syncwarp();
+    for (int i = j + 1; i < nb; i++) {
+      double part = 0.0;
+      for (int k = j + lane; k < i; k += 32) part += L[i][k] * Li[k][j];
+      part = warp_sum(part);
+      if (lane == 0) Li[i][j] = -part / L[i][i];
+      __syncwarp();
     }
   }
-  __syncthreads();
-  // R = L^T upper, R^{-1} = (L^{-1})^T
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    int i = e % nb, j = e / nb;
-    Rinv[e] = Li[j + i * nb];
-  }
+  __syncwarp();
+  // R = L^T (upper), R^{-1} = (L^{-1})^T
+  for (int j = 0; j < nb; j++)
+    for (int i = lane; i < nb; i += 32) Rinv[i + j * nb] = Li[j][i];
 }
 // Y <- Y R^{-1}  (row-parallel)
 __global__ void td_apply_rinv(double* Y, int64_t ldy, int nb, const double* Rinv, int64_t n) {
@@ -373,7 +381,7 @@ __global__ void assemble_D_kernel(const double* Q, int64_t ldq, int64_t n, int64
 
 // ------------------------------------------------------------------------------------
 static constexpr int kReorthNB = 32;
-static constexpr int64_t kGramRows = 64;
+static constexpr int64_t kGramRows = 128;
 
 void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, int window) {
   int64_t nn = std::max<int64_t>(n, 1);
@@ -403,7 +411,7 @@ static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* 
   int64_t nchunks = (n + kGramRows - 1) / kGramRows;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(td_gram_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(td_gram_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
     if (e) return e;
     attr = true;
   }
@@ -564,7 +572,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
         e = reorth_project(Y, ldq, nb, Y, ldq, nb, n, w, st);
         if (e) return e;
         KScope ks(KC_TRID_REORTH, st, 2);
-        td_chol_inv<<<1, 128, 0, st>>>(w.H, nb, w.Rinv);
+        td_chol_inv<<<1, 32, 0, st>>>(w.H, nb, w.Rinv);
         td_apply_rinv<<<(unsigned)((n + 127) / 128), 128, (size_t)nb * nb * 8, st>>>(Y, ldq, nb, w.Rinv, n);
       }
     }
