@@ -302,7 +302,11 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
     constexpr int KPB = BM / BK;   // k-steps per column block
     const int64_t nq = (p >= s.qoff) ? (p - s.qoff) / s.P + 1 : 0;
     const int64_t nk = nq * KPB;
-    auto kofs = [&](int64_t kb) -> int64_t { return (s.qoff + s.P * (kb / KPB)) * (int64_t)BM + (kb % KPB) * BK; };
+    const int qoff = s.qoff, P = s.P;
+    auto kofs = [&](int64_t kb64) -> int64_t {   // local k-step -> global column offset (32-bit math)
+      const int kb = (int)kb64;
+      return (int64_t)((qoff + P * (kb / KPB)) * BM + (kb % KPB) * BK);
+    };
     for (int st = 0; st < STAGES - 1; st++) {
       if (st < nk) TR::load_stage(g, As + st * TR::A_STAGE, Bs + st * TR::B_STAGE, m0, 0, kofs(st), tid);
       cp_async_commit();

@@ -19,7 +19,7 @@ def test_distributed_solve_matches_oracle(n):
     world = min(4, torch.cuda.device_count())
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tools", "dist_check.py"),
-           "--n", str(n)]
+           "--size", str(n)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]

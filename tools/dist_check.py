@@ -1,4 +1,4 @@
-"""Multi-GPU correctness check (torchrun --nproc-per-node N tools/dist_check.py --n 1000):
+"""Multi-GPU correctness check (torchrun --nproc-per-node N tools/dist_check.py --size 1000):
 collective distributed context (NCCL inside the library), distributed full->band, sharded
 eigenvectors; rank 0 gathers the vectors and checks them against the CPU oracle with the
 BASELINE tolerances.  Prints one JSON line on rank 0."""
@@ -16,13 +16,13 @@ import paper_1912_04062_b200 as sk  # noqa: E402
 from paper_1912_04062_b200.dist import eigpair_range, gather_columns, init_from_env  # noqa: E402
 
 p = argparse.ArgumentParser()
-p.add_argument("--n", type=int, default=1000)
+p.add_argument("--size", type=int, default=1000)
 p.add_argument("--nev", type=int, default=None)
 a = p.parse_args()
 rank, world, local = init_from_env("nccl")
 import skewgen  # noqa: E402
 
-n = a.n
+n = a.size
 nev = a.nev or n // 2
 A = skewgen.random_skew(n, n)
 ctx = sk.Context(distributed=True)
