@@ -47,7 +47,7 @@ static void plan_layout(Ctx& c, Plan& p, Arena& ar, int64_t n, int64_t nev, int 
   if (flags & (SKEW_WS_HOST_STAGING | SKEW_WS_BSE)) p.Astage = ar.take<double>((size_t)p.ldn * n);
   if (flags & SKEW_WS_BSE) p.S = ar.take<double>((size_t)std::max<int64_t>(n / 2, 1) * std::max<int64_t>(n / 2, 1));
   p.vstore = ar.take<double>((size_t)std::max<int64_t>(p.f2b.vstore_elems, 1));
-  f2b_reserve(ar, p.f2b, c.num_sms, p.fw);
+  f2b_reserve(ar, p.f2b, c.num_sms, p.fw, c.nranks);
   b2t_reserve(ar, p.b2t, vec, p.bw);
   p.alpha = ar.take<double>(std::max<int64_t>(n, 1));
   p.lam = ar.take<double>(std::max<int64_t>(nev, 1));

@@ -273,36 +273,37 @@ struct SymmArgs {
   double* X; int64_t ldx;
   int64_t m; int nb;
   int vec;
-  int P = 1, qoff = 0;   // distributed: only column blocks q = qoff (mod P) of S are local
+  // distributed (P > 1): only column blocks q = qoff (mod P) of S are local.  CTAs [0, nt)
+  // compute the row parts  Yrow_p = sum_{local q <= p} L_pq U_q  into X; CTAs
+  // [nt, nt + P*nloc) compute piece k of the column part of local column block c,
+  // -sum_{p in piece k} L_pc^T U_p, into Ycol[k] (rows of block c); a combine kernel forms
+  // X -= sum_k Ycol[k].  Splitting each column part into P pieces balances the CTAs.
+  int P = 1, qoff = 0;
+  int64_t nt = 0, nloc = 0;
+  double* Ycol = nullptr; int64_t ldy = 0;
 };
 
 template <int BM, int NB, int BK, int STAGES>
-__global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, false>::NTHREADS) symm_kernel(SymmArgs s) {
+struct SymmParts {
   using TR = GemmTile<BM, NB, BK, 32, 32, STAGES, false, false>;   // row part: A M-major
   using TC = GemmTile<BM, NB, BK, 32, 32, STAGES, true, false>;    // col part: A K-major
-  constexpr int NT = TR::NTHREADS;
-  extern __shared__ __align__(16) double smem[];
-  const int64_t p = blockIdx.x;
-  const int64_t m0 = p * BM;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp % TR::NWARP_M) * 32, wn0 = (warp / TR::NWARP_M) * 32;
-  double acc[TR::FM][TR::FN][2];
-#pragma unroll
-  for (int i = 0; i < TR::FM; i++)
-#pragma unroll
-    for (int j = 0; j < TR::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  static constexpr int NT = TR::NTHREADS;
+  using Acc = double[TR::FM][TR::FN][2];
 
-  // ---------------- row part: K over the local column blocks q <= p (q = qoff mod P)
-  {
+  // acc += sum over local column blocks q <= p of L_pq U_q   (diagonal block strictly lower)
+  __device__ static void row_part(const SymmArgs& s, double* smem, int64_t p, Acc& acc) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp % TR::NWARP_M) * 32, wn0 = (warp / TR::NWARP_M) * 32;
+    const int64_t m0 = p * BM;
     GemmArgs g;
     g.M = s.m; g.N = s.nb; g.K = smin<int64_t>(s.m, m0 + BM);
     g.A = s.S; g.lda = s.lds; g.B = s.U; g.ldb = s.ldu; g.vec = s.vec;
     double* As = smem;
     double* Bs = smem + STAGES * TR::A_STAGE;
     constexpr int KPB = BM / BK;   // k-steps per column block
-    const int64_t nq = (p >= s.qoff) ? (p - s.qoff) / s.P + 1 : 0;
-    const int64_t nk = nq * KPB;
     const int qoff = s.qoff, P = s.P;
+    const int64_t nq = (p >= qoff) ? (p - qoff) / P + 1 : 0;
+    const int64_t nk = nq * KPB;
     auto kofs = [&](int64_t kb64) -> int64_t {   // local k-step -> global column offset (32-bit math)
       const int kb = (int)kb64;
       return (int64_t)((qoff + P * (kb / KPB)) * BM + (kb % KPB) * BK);
@@ -335,28 +336,27 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
     cp_async_wait<0>();
     __syncthreads();
   }
-  // negate: the column part subtracts
-#pragma unroll
-  for (int i = 0; i < TR::FM; i++)
-#pragma unroll
-    for (int j = 0; j < TR::FN; j++) { acc[i][j][0] = -acc[i][j][0]; acc[i][j][1] = -acc[i][j][1]; }
-  // ---------------- column part: K (rows of S) in [m0, m); A(mm, k) = S[k, m0+mm]
-  {
+
+  // acc += sum over rows k in [kbeg, kend) of L_{k, c-block}^T U_k  (rows k > column index)
+  __device__ static void col_part(const SymmArgs& s, double* smem, int64_t c, int64_t kbeg, int64_t kend, Acc& acc) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp % TR::NWARP_M) * 32, wn0 = (warp / TR::NWARP_M) * 32;
+    const int64_t m0 = c * BM;
     GemmArgs g;
     g.M = s.m; g.N = s.nb; g.K = s.m;
     g.A = s.S; g.lda = s.lds; g.B = s.U; g.ldb = s.ldu; g.vec = s.vec;
     double* As = smem;
     double* Bs = smem + STAGES * TC::A_STAGE;
-    const int64_t nk = (((p - s.qoff) % s.P + s.P) % s.P == 0) ? (s.m - m0 + BK - 1) / BK : 0;   // local column p
+    const int64_t nk = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
     for (int st = 0; st < STAGES - 1; st++) {
-      if (st < nk) TC::load_stage(g, As + st * TC::A_STAGE, Bs + st * TC::B_STAGE, m0, 0, m0 + st * BK, tid);
+      if (st < nk) TC::load_stage(g, As + st * TC::A_STAGE, Bs + st * TC::B_STAGE, m0, 0, kbeg + st * BK, tid);
       cp_async_commit();
     }
     for (int64_t kb = 0; kb < nk; kb++) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
       const int cs = (int)(kb % STAGES);
-      const int64_t k0 = m0 + kb * BK;
+      const int64_t k0 = kbeg + kb * BK;
       if (k0 < m0 + BM) {   // diagonal tile: keep k > m0+mm only
         double* a = As + cs * TC::A_STAGE;
         for (int e = tid; e < BK * BM; e += NT) {
@@ -368,24 +368,79 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
       int64_t pf = kb + STAGES - 1;
       if (pf < nk) {
         int ps = (int)(pf % STAGES);
-        TC::load_stage(g, As + ps * TC::A_STAGE, Bs + ps * TC::B_STAGE, m0, 0, m0 + pf * BK, tid);
+        TC::load_stage(g, As + ps * TC::A_STAGE, Bs + ps * TC::B_STAGE, m0, 0, kbeg + pf * BK, tid);
       }
       cp_async_commit();
       TC::mma_stage(As + cs * TC::A_STAGE, Bs + cs * TC::B_STAGE, acc, wm0, wn0, lane);
     }
     cp_async_wait<0>();
+    __syncthreads();
   }
-  const int gq = lane >> 2, t = lane & 3;
+
+  __device__ static void store(const SymmArgs& s, double* out, int64_t ldo, int64_t m0, double sign, Acc& acc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm0 = (warp % TR::NWARP_M) * 32, wn0 = (warp / TR::NWARP_M) * 32;
+    const int gq = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int i = 0; i < TR::FM; i++)
+#pragma unroll
+      for (int j = 0; j < TR::FN; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          int64_t mm = m0 + wm0 + 8 * i + gq;
+          int nn = wn0 + 8 * j + 2 * t + h;
+          if (mm < s.m && nn < s.nb) out[SK_IDX(mm, nn, ldo)] = sign * acc[i][j][h];
+        }
+  }
+};
+
+// a3 skew-SYMM  X = S U,  S = L - L^T (L = strictly lower part of A[r0:, r0:]).
+// One device: CTA p runs ONE K loop over the row part L[p, 0:(p+1)BM] U and the column part
+// -L[pBM:, p]^T U, so every lower tile is read twice overall and each CTA's K extent is
+// n + BM (balanced).  Distributed: see SymmArgs.
+template <int BM, int NB, int BK, int STAGES>
+__global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, false>::NTHREADS) symm_kernel(SymmArgs s) {
+  using SP = SymmParts<BM, NB, BK, STAGES>;
+  using TR = typename SP::TR;
+  extern __shared__ __align__(16) double smem[];
+  double acc[TR::FM][TR::FN][2];
 #pragma unroll
   for (int i = 0; i < TR::FM; i++)
 #pragma unroll
-    for (int j = 0; j < TR::FN; j++)
+    for (int j = 0; j < TR::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int64_t bid = blockIdx.x;
+  if (s.P == 1) {
+    SP::row_part(s, smem, bid, acc);
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        int64_t mm = m0 + wm0 + 8 * i + gq;
-        int nn = wn0 + 8 * j + 2 * t + h;
-        if (mm < s.m && nn < s.nb) s.X[SK_IDX(mm, nn, s.ldx)] = -acc[i][j][h];
-      }
+    for (int i = 0; i < TR::FM; i++)
+#pragma unroll
+      for (int j = 0; j < TR::FN; j++) { acc[i][j][0] = -acc[i][j][0]; acc[i][j][1] = -acc[i][j][1]; }
+    SP::col_part(s, smem, bid, bid * BM, s.m, acc);
+    SP::store(s, s.X, s.ldx, bid * BM, -1.0, acc);
+  } else if (bid < s.nt) {
+    SP::row_part(s, smem, bid, acc);
+    SP::store(s, s.X, s.ldx, bid * BM, 1.0, acc);
+  } else {
+    const int64_t w = bid - s.nt, i = w / s.P, k = w % s.P;
+    const int64_t c = s.qoff + (int64_t)s.P * i;
+    const int64_t nrb = s.nt - c;                          // row blocks c .. nt-1
+    const int64_t b0 = c + (nrb * k) / s.P, b1 = c + (nrb * (k + 1)) / s.P;
+    SP::col_part(s, smem, c, b0 * BM, smin<int64_t>(s.m, b1 * BM), acc);
+    SP::store(s, s.Ycol + (size_t)k * s.ldy * s.nb, s.ldy, c * BM, 1.0, acc);
+  }
+}
+
+// X -= sum_k Ycol[k] on the rows of the local column blocks (distributed skew-SYMM)
+__global__ void symm_combine_kernel(double* X, int64_t ldx, const double* Ycol, int64_t ldy, int npieces, int64_t m,
+                                    int nb, int BM, int P, int qoff) {
+  const int64_t col = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = i / BM;
+    if (((blk - qoff) % P + P) % P != 0) continue;
+    double sacc = 0.0;
+    for (int k = 0; k < npieces; k++) sacc += Ycol[(size_t)k * ldy * nb + i + col * ldy];
+    X[i + col * ldx] -= sacc;
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -457,7 +512,7 @@ __global__ void pq_build_kernel(const double* V, int64_t ldv, int64_t m, int kb,
 static constexpr int kSymmBM = 64, kSymmBK = 16, kSymmStages = 2;
 static constexpr int kWRows = 256;
 
-void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w) {
+void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w, int P) {
   int64_t n = L.n, b = L.b;
   int64_t np = std::max<int64_t>(L.npanel, 1);
   w.tau = ar.take<double>(np * b);
@@ -472,6 +527,7 @@ void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w) {
   w.Q = ar.take<double>(ldn * 2 * b);
   w.zpart = ar.take<double>(((n + kWRows - 1) / kWRows + 2) * b * b);
   w.Mb = ar.take<double>(b * b);
+  if (P > 1) w.Ycol = ar.take<double>((size_t)P * ldn * b);
 }
 
 static int panel_grid(int64_t m, int nsm) {
@@ -554,8 +610,20 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
       if (e) return e;
       set = true;
     }
-    KScope ks(KC_SYMM, st);
-    symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)((m + kSymmBM - 1) / kSymmBM), TR::NTHREADS, smem, st>>>(s);
+    const int64_t nt = (m + kSymmBM - 1) / kSymmBM;
+    int64_t grid = nt;
+    if (d.P > 1) {
+      s.nt = nt;
+      s.nloc = (nt > qoff) ? (nt - qoff + d.P - 1) / d.P : 0;
+      s.Ycol = w.Ycol; s.ldy = ldn;
+      grid = nt + (int64_t)d.P * s.nloc;
+    }
+    KScope ks(KC_SYMM, st, d.P > 1 ? 2 : 1);
+    symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)grid, TR::NTHREADS, smem, st>>>(s);
+    if (d.P > 1) {
+      dim3 cg((unsigned)std::min<int64_t>((m + 255) / 256, 64), (unsigned)b);
+      symm_combine_kernel<<<cg, 256, 0, st>>>(Wp, ldn, w.Ycol, ldn, d.P, m, b, kSymmBM, d.P, qoff);
+    }
   }
   if (d.P > 1) {   // Y = sum over ranks of the partial skew-SYMM products (NVLink allreduce)
     ncclResult_t r = ncclAllReduce(Wp, Wp, (size_t)ldn * b, ncclDouble, ncclSum, (ncclComm_t)d.comm, st);

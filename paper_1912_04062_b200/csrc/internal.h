@@ -130,6 +130,7 @@ struct F2BWork {
   double* Q = nullptr;       // n x 2b
   double* zpart = nullptr;   // V^T X partials
   double* Mb = nullptr;      // b x b
+  double* Ycol = nullptr;    // distributed skew-SYMM column-part pieces (P x n x b)
 };
 
 struct B2TLayout {
@@ -181,7 +182,7 @@ struct Dist {
 };
 
 // f2b.cu
-void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w);
+void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w, int P = 1);
 // returns cudaErrorUnknown + sets *nccl_err on an NCCL failure
 cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, const F2BWork& w, int nsm,
                     cudaStream_t st, const Dist& d, int* nccl_err);
