@@ -11,7 +11,7 @@
 //   right to the block below rows [r+L, r+L+b) x cols [r, r+L).
 // The band is kept in lower band storage with 2b+2 rows (the bulge reaches 2b-1).
 // Sweeps run concurrently on a persistent cooperative grid: sweep s+1 starts task t
-// once sweep s has finished task t+3 (their index ranges are then disjoint).
+// once sweep s has finished task t+1 (see the chase kernel for why lag 2 is enough).
 //
 // BT2 (Algorithm 1 step 4): X <- Q2 X.  The reflectors of k
 // consecutive sweeps at one chase position t form G = H_s0 ... H_{s0+k-1} = I - V T V^T
@@ -42,180 +42,273 @@ struct ChaseArgs {
 
 __device__ __forceinline__ int64_t chase_ntask(int64_t n, int b, int64_t s) { return 1 + (n - 3 - s) / b; }
 
+// Chase kernel.  Persistent cooperative grid, one sweep per CTA at a time, the tasks above
+// in shared-memory column slots:
+//  * Sweep s task t needs sweep s-1 tasks 0..t+1 complete (lag 2 instead of 3).  It shares
+//    exactly one entry with s-1's task t+2: A(r', col'), r' = s+(t+2)b, col' = r'-b, which
+//    task t+2's Householder overwrites with beta and never touches again; every other entry
+//    of the two tasks is disjoint, as is s task t from sweep s-1 tasks >= t+3 and sweep s-2
+//    tasks >= t+3 (checked exhaustively on access sets for small n, b and numerically
+//    against the sequential order).  Each sweep computes the Householder of task t+1 as
+//    soon as column 0 of task t's block below is final (during task t's update) and stores
+//    beta to global memory before task t completes, so "s-1 tasks 0..t+1 complete" also
+//    covers the shared entry.  The per-sweep critical chain is two tasks.
+//  * 12 compute warps + 1 auxiliary warp.  Warp 0 polls and, in the update, takes only
+//    diagonal column 0 and then the next Householder; the auxiliary warp publishes task
+//    completion (fence + flag) and stores the next reflector while the compute warps go on
+//    to the next task.  The diagonal and left blocks are final after the update and go from
+//    registers straight to global memory; only the block below stays in shared memory
+//    (task t+1's left block).
+constexpr int kChaseCW = 12;                       // compute warps
+constexpr int kChaseThreads = (kChaseCW + 1) * 32;   // + 1 auxiliary warp
+
 template <int MAXB>
-__global__ void __launch_bounds__(256) chase_kernel(ChaseArgs a) {
-  // Shared window: a ring of 2b column slots (+1 for the t = 0 column) in band storage,
-  // slot(c) = (c - s - 1) mod 2b.  Task t of sweep s works on columns [r-b, r+b); the
-  // block below its diagonal block (E_t, rows [r+L, e)) is exactly task t+1's left block,
-  // so it stays in shared memory (loaded once, written back once, as task t+1's final
-  // left block); each task loads only its diagonal-block columns [r, r+L) and writes back
-  // its (final) left block and diagonal block.
+__global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(ChaseArgs a) {
   extern __shared__ __align__(16) double W[];
-  __shared__ double vs[MAXB], ws[MAXB], zs[MAXB], ys[MAXB], sc[4];
+  __shared__ double vsb[2][MAXB];   // reflector of task t in vsb[t & 1], tau/beta in scb
+  __shared__ double scb[2][2];
+  __shared__ double red[2][3 * MAXB];
+  __shared__ double uz[2 * MAXB], vv[2 * MAXB], yv[MAXB];
+  __shared__ int dbase[MAXB], lbase[MAXB];
   const int b = a.b;
-  const int LDW = 2 * b + 2;   // LDW - 1 odd: the strided skew reads of D are conflict-free
+  const int LDW = 2 * b + 2, B2 = 2 * b;
   const int64_t n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NCT = kChaseCW * 32;   // compute threads
   const bool prof = a.dbg != nullptr && blockIdx.x == 0 && tid == 0;
   long long t_wait = 0, t_work = 0, ntasks = 0, tk = 0, tph[5] = {0, 0, 0, 0, 0}, tp = 0;
-#define CH_TS(i) do { if (prof) { long long _n = clock64(); tph[i] += _n - tp; tp = _n; } } while (0)
+#define C2_TS(i) do { if (prof) { long long _n = clock64(); tph[i] += _n - tp; tp = _n; } } while (0)
   for (int64_t s = blockIdx.x; s < n - 2; s += gridDim.x) {
-    const int64_t nt = chase_ntask(n, b, s);
-    const int64_t ntprev = (s > 0) ? chase_ntask(n, b, s - 1) : 0;
-    for (int64_t t = 0; t < nt; t++) {
-      // ---- sweep s task t may run once sweep s-1 finished tasks 0..t+2 (their entry sets
-      //      are then disjoint from this task's; checked against the sequential order)
-      if (prof) tk = clock64();
-      if (s > 0) {
-        if (tid == 0) {
-          const int need = (int)smin<int64_t>(t + 3, ntprev);
-          volatile int* pr = a.progress + (s - 1);
-          while (*pr < need) { __nanosleep(32); }
-          __threadfence();
-        }
-        __syncthreads();
+    const int nt = (int)chase_ntask(n, b, s);
+    const int ntprev = (s > 0) ? (int)chase_ntask(n, b, s - 1) : 0;
+    const int64_t gbase = a.gofs[s / a.k2];
+    const int cpos = (int)(s % a.k2);
+    volatile int* prme = a.progress + s;
+    // task geometry: left column col, reflector rows [r, r+L), block rows [c, e)
+    auto geom = [&](int t, int64_t& col, int64_t& r, int& L) {
+      if (t == 0) { col = s; r = s + 1; L = (int)smin<int64_t>(b, n - 1 - s); }
+      else { col = s + 1 + (int64_t)(t - 1) * b; r = col + b; L = (int)smin<int64_t>(b, n - r); }
+    };
+    // Householder of x = W[xoff + 0 .. L) (dlarfg convention) by one warp -> vsb[p], scb[p]
+    auto house = [&](int xoff, int L, int p) {
+      double s2 = 0.0;
+      for (int i = 1 + lane; i < L; i += 32) { const double x = W[xoff + i]; s2 += x * x; }
+      s2 = warp_sum(s2);
+      const double x0 = W[xoff];
+      double beta, tau, scal;
+      if (s2 == 0.0) { beta = x0; tau = 0.0; scal = 0.0; }
+      else {
+        const double nrm = sqrt(x0 * x0 + s2);
+        beta = (x0 >= 0.0) ? -nrm : nrm;
+        tau = (beta - x0) / beta;
+        scal = 1.0 / (x0 - beta);
       }
-      if (prof) { long long now = clock64(); t_wait += now - tk; tk = now; tp = now; ntasks++; }
-      int64_t col, r, L;
-      if (t == 0) { col = s; r = s + 1; L = smin<int64_t>(b, n - 1 - s); }
-      else { col = s + 1 + (t - 1) * b; r = col + b; L = smin<int64_t>(b, n - r); }
+      for (int i = lane; i < L; i += 32) vsb[p][i] = (i == 0) ? 1.0 : W[xoff + i] * scal;
+      if (lane == 0) { scb[p][0] = tau; scb[p][1] = beta; }
+    };
+    // final left column of task t (beta, 0, ...) and its reflector for BT2, by one warp
+    auto store_col_refl = [&](int t) {
+      int64_t col, r;
+      int L;
+      geom(t, col, r, L);
+      const int p = t & 1;
+      double* gp = a.AB + col * a.ldab + (r - col);
+      const double beta = scb[p][1];
+      for (int i = lane; i < L; i += 32) __stcg(&gp[i], i == 0 ? beta : 0.0);
+      double* dst = a.qv + ((gbase + t) * a.k2 + cpos) * b;
+      for (int i = lane; i < L; i += 32) dst[i] = vsb[p][i];
+      if (lane == 0) a.qtau[(gbase + t) * a.k2 + cpos] = scb[p][0];
+    };
+    for (int t = 0; t < nt; t++) {
+      int64_t col, r;
+      int L;
+      geom(t, col, r, L);
       const int64_t e = smin<int64_t>(n, r + L + b);
-      const int nl = (int)(r - col);          // columns of the left block (1 for t = 0)
-      const int ne = (int)(e - r - L);         // rows of the block below
+      const int nl = (int)(r - col);
+      const int ne = (int)(e - r - L);
       const bool last = (t + 1 == nt);
-      // column slots (32-bit, no division in the inner loops): left columns col + cc, and
-      // the diagonal-block columns r + j
-      const int B2 = 2 * b;
+      const int p = t & 1;
+      const double* vs = vsb[p];
       const int sr0 = (int)((r - s - 1) % B2);
       const int sc0 = (t == 0) ? B2 : (int)((col - s - 1) % B2);
       auto sl_left = [&](int cc) -> int { if (t == 0) return B2; int x = sc0 + cc; return x >= B2 ? x - B2 : x; };
       auto sl_diag = [&](int j) -> int { int x = sr0 + j; return x >= B2 ? x - B2 : x; };
-      // ---- load: t = 0 also the left column s; always the columns [r, r+L) rows [c, e).
-      //      16-byte L2-coherent cp.async on even-widened band offsets (widened elements
-      //      are only read, never written back).
-      if (t == 0 && warp == 7) {
-        const int d0 = (int)(r - col) & ~1, d1 = (int)(r + L - col);
-        for (int d = d0 + 2 * lane; d < d1; d += 64) cp_async16(&W[B2 * LDW + d], &a.AB[d + col * a.ldab], 16);
-      }
-      for (int j = warp; j < L; j += 8) {
-        const int64_t c = r + j;
-        const int d1 = (int)(e - c);
-        const int sj = sl_diag(j);
-        for (int d = 2 * lane; d < d1; d += 64) cp_async16(&W[sj * LDW + d], &a.AB[d + c * a.ldab], 16);
-      }
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncthreads();
-      CH_TS(0);
-      // ---- (a) Householder of x = A[r:r+L, col]  (dlarfg convention)
-      const int scol = sl_left(0);
-      if (warp == 0) {
-        double s2 = 0.0;
-        for (int i = 1 + lane; i < L; i += 32) { double x = W[scol * LDW + (r + i - col)]; s2 += x * x; }
-        s2 = warp_sum(s2);
-        double x0 = W[scol * LDW + (r - col)];
-        double beta, tau, scal;
-        if (s2 == 0.0) { beta = x0; tau = 0.0; scal = 0.0; }
-        else {
-          double nrm = sqrt(x0 * x0 + s2);
-          beta = (x0 >= 0.0) ? -nrm : nrm;
-          tau = (beta - x0) / beta;
-          scal = 1.0 / (x0 - beta);
+      if (warp < kChaseCW) {
+        if (prof) tk = clock64();
+        // ---- (1) dependency: sweep s-1 tasks 0..t+1 complete (warp 0 polls, whole warp)
+        if (warp == 0 && s > 0) {
+          const int need = min(t + 2, ntprev);
+          volatile int* pr = a.progress + (s - 1);
+          while (*pr < need) { }
+          __threadfence();
         }
-        for (int i = lane; i < L; i += 32) {
-          double v = (i == 0) ? 1.0 : W[scol * LDW + (r + i - col)] * scal;
-          vs[i] = v;
-          W[scol * LDW + (r + i - col)] = (i == 0) ? beta : 0.0;
+        named_bar(1, NCT);
+        if (prof) { long long now = clock64(); t_wait += now - tk; tk = now; tp = now; ntasks++; }
+        // ---- (2) load the diagonal-block columns [r, r+L), rows [c, e) (t = 0: also column s)
+        if (t == 0 && warp == 0) {
+          const int d1 = (int)(r + L - col);
+          for (int d = 2 * lane; d < d1; d += 64) cp_async16(&W[B2 * LDW + d], &a.AB[d + col * a.ldab], 16);
         }
-        if (lane == 0) sc[0] = tau;
-      }
-      __syncthreads();
-      CH_TS(1);
-      const double tau = sc[0];
-      {   // store the reflector (v zero-padded to b by the initial memset)
-        const int64_t blk = s / a.k2, c = s % a.k2;
-        const int64_t gidx = a.gofs[blk] + t;
-        double* dst = a.qv + (gidx * a.k2 + c) * b;
-        for (int i = tid; i < L; i += 256) dst[i] = vs[i];
-        if (tid == 0) a.qtau[gidx * a.k2 + c] = tau;
-      }
-      if (tau != 0.0) {
-        // ---- y = tau v^T A[r:r+L, c] (left columns), w = tau D v, z = tau E v: 4 threads per item
-        const int item = tid >> 2, part = tid & 3;
-        double sy = 0.0, sw = 0.0, sz = 0.0;   // shuffles below run on all lanes (full mask)
-        if (item >= 1 && item < nl) {
-          const int sl = sl_left(item), d0 = nl - item;   // row r sits at offset r - c
-#pragma unroll 4
-          for (int i = part; i < L; i += 4) sy += vs[i] * W[sl * LDW + d0 + i];
-        }
-        if (item < L) {
-          for (int j = part; j < item; j += 4) sw += W[sl_diag(j) * LDW + (item - j)] * vs[j];
-          const int sr = sl_diag(item);
-          for (int j = item + 1 + part; j < L; j += 4) sw -= W[sr * LDW + (j - item)] * vs[j];
-        }
-        if (item < ne) {
-#pragma unroll 4
-          for (int j = part; j < L; j += 4) sz += W[sl_diag(j) * LDW + (L + item - j)] * vs[j];
-        }
-#pragma unroll
-        for (int o = 1; o <= 2; o <<= 1) {
-          sy += __shfl_xor_sync(0xffffffffu, sy, o);
-          sw += __shfl_xor_sync(0xffffffffu, sw, o);
-          sz += __shfl_xor_sync(0xffffffffu, sz, o);
-        }
-        if (part == 0) {
-          if (item < nl) ys[item] = tau * sy;
-          if (item < L) ws[item] = tau * sw;
-          if (item < ne) zs[item] = tau * sz;
-        }
-        __syncthreads();
-        CH_TS(2);
-        // ---- left block -= v y^T;  D_ij += v_i w_j - w_i v_j (i > j);  E_ij -= z_i v_j
-#pragma unroll 4
-        for (int cc = 1 + warp; cc < nl; cc += 8) {
-          const int sl = sl_left(cc), d0 = nl - cc;
-          const double yc = ys[cc];
-          for (int i = lane; i < L; i += 32) W[sl * LDW + d0 + i] -= yc * vs[i];
-        }
-#pragma unroll 4
-        for (int j = warp; j < L; j += 8) {
+        for (int j = warp; j < L; j += kChaseCW) {
+          const int64_t c = r + j;
+          const int d1 = (int)(e - c);
           const int sj = sl_diag(j);
-          const double vj = vs[j], wj = ws[j];
-          for (int i = j + 1 + lane; i < L; i += 32) W[sj * LDW + (i - j)] += vs[i] * wj - ws[i] * vj;
-          for (int i = lane; i < ne; i += 32) W[sj * LDW + (L + i - j)] -= zs[i] * vj;
+          for (int d = 2 * lane; d < d1; d += 64) cp_async16(&W[sj * LDW + d], &a.AB[d + c * a.ldab], 16);
         }
+        // smem offset tables: element (row i, diagonal column j) at dbase[j] + i, (row i,
+        // left column cc) at lbase[cc] + i, block-relative rows
+        if (tid < L) dbase[tid] = sl_diag(tid) * LDW - tid;
+        else if (tid >= MAXB && tid - MAXB < nl) lbase[tid - MAXB] = sl_left(tid - MAXB) * LDW + nl - (tid - MAXB);
+        cp_async_commit();
+        cp_async_wait<0>();
+        named_bar(1, NCT);
+        if (t == 0) {   // first task of the sweep: its Householder needs column s
+          if (warp == 0) { house(B2 * LDW + 1, L, p); __syncwarp(); store_col_refl(0); }
+          named_bar(1, NCT);
+        }
+        C2_TS(0);
+        const double tau = scb[p][0];
+        // ---- (3) y = v^T (left block), w = D v (skew, lower storage), z = E v: one item per
+        //      thread pair (every other j), four independent chains, branch-free bodies
+        const int part = tid / (3 * MAXB), it = tid % (3 * MAXB);
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        auto dot4 = [&](auto&& f) {
+          int j = part;
+          for (; j + 6 < L; j += 8) { acc0 += f(j); acc1 += f(j + 2); acc2 += f(j + 4); acc3 += f(j + 6); }
+          for (; j < L; j += 2) acc0 += f(j);
+        };
+        if (it < b) {
+          const int cc = it;
+          if (cc >= 1 && cc < nl) {
+            const int base = lbase[cc];
+            dot4([&](int i) { return vs[i] * W[base + i]; });
+          }
+        } else if (it < 2 * b) {
+          const int i = it - b;
+          if (i < L) {
+            const int si = dbase[i];
+            // w_i = sum_{j<i} D(i,j) v_j - sum_{j>i} D(j,i) v_j with the same j on every lane:
+            // lower reads (row i) contiguous over lanes, upper reads (column i) at the odd
+            // stride LDW-1; j == i reads the stored zero diagonal
+            dot4([&](int j) {
+              const bool lo = j < i;
+              return W[lo ? dbase[j] + i : si + j] * (lo ? vs[j] : -vs[j]);
+            });
+          }
+        } else if (it < 3 * b) {
+          const int i = it - 2 * b;
+          if (i < ne) dot4([&](int j) { return W[dbase[j] + L + i] * vs[j]; });
+        }
+        if (it < 3 * b) red[part][it] = (acc0 + acc1) + (acc2 + acc3);
+        named_bar(1, NCT);
+        // uz = [tau w (rows of D) | tau z (rows of E) | 0], vv = [v | 0], yv = tau y
+        if (tid < 2 * b) {
+          const int i = tid;
+          uz[i] = (i < L) ? tau * (red[0][b + i] + red[1][b + i])
+                          : (i - L < ne ? tau * (red[0][2 * b + i - L] + red[1][2 * b + i - L]) : 0.0);
+          vv[i] = (i < L) ? vs[i] : 0.0;
+        } else if (tid < 3 * b) {
+          const int i = tid - 2 * b;
+          yv[i] = tau * (red[0][i] + red[1][i]);
+        }
+        named_bar(1, NCT);
+        C2_TS(1);
+        // ---- (4) left block -= v y^T; D += v w^T - w v^T (lower); E -= z v^T.  Left and D
+        //      are final: registers -> global.  E stays in smem (task t+1's left block).
+        //      Lane owns rows lane + 32k (coefficients in registers); all loads first
+        //      (in-slot, always safe), predicated stores.  Warp 0 does diagonal column 0
+        //      only, then the Householder of task t+1 from that column's block-below part.
+        const int ncl = nl - 1;
+        const int iend = L + ne;
+        double vr[2 * MAXB / 32], ur[2 * MAXB / 32];
+#pragma unroll
+        for (int k = 0; k < 2 * MAXB / 32; k++) { vr[k] = vv[lane + 32 * k]; ur[k] = uz[lane + 32 * k]; }
+        double* const gd0 = a.AB + r * a.ldab;   // + j*(ldab-1): diagonal of column r+j
+        const int ldm1 = (int)a.ldab - 1;
+        auto diag_cols = [&](int j0, int j1, bool h1) {
+          const int b0 = dbase[j0], b1 = dbase[j1];
+          const double v0 = vs[j0], w0 = uz[j0], v1 = vs[j1], w1 = uz[j1];
+          double x0[2 * MAXB / 32], x1[2 * MAXB / 32];
+#pragma unroll
+          for (int k = 0; k < 2 * MAXB / 32; k++) { x0[k] = W[b0 + lane + 32 * k]; x1[k] = W[b1 + lane + 32 * k]; }
+          double* g0 = gd0 + j0 * ldm1;
+          double* g1 = gd0 + j1 * ldm1;
+#pragma unroll
+          for (int k = 0; k < 2 * MAXB / 32; k++) {
+            const int i = lane + 32 * k;
+            const double z0 = x0[k] + vr[k] * w0 - ur[k] * v0;
+            const double z1 = x1[k] + vr[k] * w1 - ur[k] * v1;
+            const bool e0 = i > j0 && i < iend, e1 = h1 && i > j1 && i < iend;
+            const bool isE = i >= L;
+            const bool gst = !isE || last;
+            if (e0 && isE) W[b0 + i] = z0;
+            if (e1 && isE) W[b1 + i] = z1;
+            if (e0 && gst) __stcg(&g0[i], z0);
+            if (e1 && gst) __stcg(&g1[i], z1);
+          }
+        };
+        if (warp == 0) {
+          diag_cols(0, 0, false);
+          if (!last) {
+            // Householder of task t+1: x = rows [r+b, r+b+L1) of column r = this column's
+            // block-below part (final now); beta goes to global memory before task t completes
+            __syncwarp();
+            int64_t col1, r1;
+            int L1;
+            geom(t + 1, col1, r1, L1);
+            house(dbase[0] + b, L1, p ^ 1);
+            __syncwarp();
+            if (lane == 0) __stcg(a.AB + col1 * a.ldab + (r1 - col1), scb[p ^ 1][1]);
+          }
+        } else {
+          const int w = warp - 1;   // 11 warps: left columns, then diagonal columns 1..L-1
+          constexpr int NW = kChaseCW - 1;
+          double vl[MAXB / 32];
+#pragma unroll
+          for (int k = 0; k < MAXB / 32; k++) vl[k] = vs[lane + 32 * k];
+          double* const gl0 = a.AB + col * a.ldab + nl;   // + cc*(ldab-1): row r of column col+cc
+          for (int q = w; q < ncl; q += 2 * NW) {
+            const int c0 = q + 1, c1 = min(q + 1 + NW, nl - 1);
+            const bool h1 = q + NW < ncl;
+            const int b0 = lbase[c0], b1 = lbase[c1];
+            const double y0 = yv[c0], y1 = yv[c1];
+            double x0[MAXB / 32], x1[MAXB / 32];
+#pragma unroll
+            for (int k = 0; k < MAXB / 32; k++) { x0[k] = W[b0 + lane + 32 * k]; x1[k] = W[b1 + lane + 32 * k]; }
+            double* g0 = gl0 + c0 * ldm1;
+            double* g1 = gl0 + c1 * ldm1;
+#pragma unroll
+            for (int k = 0; k < MAXB / 32; k++) {
+              const int i = lane + 32 * k;
+              const bool ok = i < L;
+              const double z0 = x0[k] - y0 * vl[k], z1 = x1[k] - y1 * vl[k];
+              if (ok) __stcg(&g0[i], z0);
+              if (ok && h1) __stcg(&g1[i], z1);
+            }
+          }
+          // diagonal columns 1..L-1; the count of left columns shifts the start so the
+          // warps stay balanced
+          const int q0 = (ncl + w) % NW;
+          for (int q = q0; q < L - 1; q += 2 * NW) {
+            const int j0 = 1 + q, j1 = min(1 + q + NW, L - 1);
+            diag_cols(j0, j1, q + NW < L - 1);
+          }
+        }
+        C2_TS(2);
       }
       __syncthreads();
-      CH_TS(3);
-      // ---- write back the final entries: the left block (rows [r, r+L) of columns [col, r)),
-      //      the diagonal block, and -- on the sweep's last task -- the block below.
-      for (int cc = warp; cc < nl; cc += 8) {
-        const int64_t c = col + cc;
-        const int sl = sl_left(cc);
-        double* gp = a.AB + c * a.ldab + (r - c);
-        const double* wp = W + sl * LDW + (int)(r - c);
-        for (int i = lane; i < L; i += 32) __stcg(&gp[i], wp[i]);
+      if (warp == kChaseCW) {
+        // ---- auxiliary warp: task t complete (all its writes precede the barrier, incl. the
+        //      beta of task t+1), then the next task's final left column and reflector
+        if (lane == 0) { __threadfence(); *prme = t + 1; }
+        if (!last) { __syncwarp(); store_col_refl(t + 1); }
       }
-      for (int j = warp; j < L; j += 8) {
-        const int64_t c = r + j;
-        const int sj = sl_diag(j);
-        const int len = (int)((last ? e : r + L) - c);
-        double* gp = a.AB + c * a.ldab;
-        const double* wp = W + sj * LDW;
-        for (int i = lane; i < len; i += 32) __stcg(&gp[i], wp[i]);
-      }
-      __syncthreads();
-      if (tid == 0) {   // barrier, then one GPU-scope fence + flag (the grid-barrier pattern)
-        __threadfence();
-        volatile int* pr = a.progress + s;
-        *pr = (int)(t + 1);
-      }
-      CH_TS(4);
+      C2_TS(3);
       if (prof) t_work += clock64() - tk;
     }
   }
   if (prof) { a.dbg[0] = t_wait; a.dbg[1] = t_work; a.dbg[2] = ntasks; for (int i = 0; i < 5; i++) a.dbg[3 + i] = tph[i]; }
-#undef CH_TS
+#undef C2_TS
 }
 
 // extract Lemma-1 alpha_k = -T[k+1, k] from the final band
@@ -884,9 +977,9 @@ void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w) {
   w.gofs = ar.take<int64_t>(std::max<int64_t>(L.nblk, 1));
 }
 
-static int chase_grid(int64_t n, int b, int nsm) {
-  // concurrently active sweeps ~ (n/b)/3; never more CTAs than can be co-resident
-  int64_t act = std::max<int64_t>(1, (n / std::max(b, 1)) / 3 + 1);
+static int chase_grid(int64_t n, int b, int nsm, int lag) {
+  // concurrently active sweeps ~ (n/b)/lag; never more CTAs than can be co-resident
+  int64_t act = std::max<int64_t>(1, (n / std::max(b, 1)) / lag + 1);
   return (int)std::max<int64_t>(1, std::min<int64_t>(act, nsm));
 }
 
@@ -911,23 +1004,24 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
       a.qv = w.qv; a.qtau = w.qtau; a.gofs = w.gofs;
       a.dbg = nullptr;
       if (getenv("SKEWEIG_CHASE_DBG")) {   // debug instrumentation only
-        cudaError_t me = cudaMalloc(&a.dbg, 8 * sizeof(long long));
+        cudaError_t me = cudaMalloc(&a.dbg, 48 * sizeof(long long));
         if (me) { fprintf(stderr, "[chase dbg] cudaMalloc failed: %s\n", cudaGetErrorString(me)); a.dbg = nullptr; }
+        else cudaMemsetAsync(a.dbg, 0, 48 * sizeof(long long), st);
       }
-      int G = chase_grid(n, L.b, nsm);
+      int G = chase_grid(n, L.b, nsm, 2);
+      if (const char* gg = getenv("SKEWEIG_CHASE_G")) G = std::max(1, std::min(G, atoi(gg)));   // experiments
       size_t smem = (size_t)(2 * L.b + 1) * (2 * L.b + 2) * sizeof(double);
-      e = cudaFuncSetAttribute(chase_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e) return e;
       void* args[] = {&a};
-      e = cudaLaunchCooperativeKernel((void*)chase_kernel<128>, dim3(G), dim3(256), args, smem, st);
+      e = cudaFuncSetAttribute(chase_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+      e = cudaLaunchCooperativeKernel((void*)chase_kernel<64>, dim3(G), dim3(kChaseThreads), args, smem, st);
       if (e) return e;
       if (a.dbg) {
-        long long h[8];
+        long long h[48];
         cudaMemcpyAsync(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        fprintf(stderr, "[chase dbg] G=%d tasks(cta0)=%lld  per task: wait %.0f work %.0f (load %.0f house %.0f "
-                "w/z %.0f rank2 %.0f store %.0f) cycles\n", G, h[2], (double)h[0] / h[2], (double)h[1] / h[2],
-                (double)h[3] / h[2], (double)h[4] / h[2], (double)h[5] / h[2], (double)h[6] / h[2], (double)h[7] / h[2]);
+        fprintf(stderr, "[chase dbg] G=%d tasks(cta0)=%lld  per task: wait %.0f work %.0f (load %.0f products %.0f "
+                "update %.0f end %.0f) cycles\n", G, h[2], (double)h[0] / h[2], (double)h[1] / h[2],
+                (double)h[3] / h[2], (double)h[4] / h[2], (double)h[5] / h[2], (double)h[6] / h[2]);
         cudaFree(a.dbg);
       }
     }
