@@ -298,7 +298,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   tstart(ctx, ST_TRID);
   int64_t nfail = 0;
   int64_t vlo = k0;
-  CK(trid_run(n, p.alpha, nev, p.lam, vec ? p.Q : nullptr, p.ldn, p.tw, c.prm, &nfail, st, k0, k1, &vlo),
+  CK(trid_run(n, p.alpha, nev, p.lam, vec ? p.Q : nullptr, p.ldn, p.tw, c.prm, &nfail, st, k0, k1, &vlo, &d),
      "tridiagonal");
   c.last_nfail = nfail;
   if (vec) {

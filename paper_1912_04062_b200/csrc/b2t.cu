@@ -420,258 +420,11 @@ struct BT2Cfg {
   static constexpr int XS = NB * LDX, GS = Gp::ELEMS, ZS = NB * LDZ;
   static constexpr size_t SMEM = (size_t)(XS + 2 * GS + ZS) * sizeof(double) + 2 * sizeof(uint64_t);
   static_assert(LDX % 16 == 4 && LDW % 16 == 4 && LDZ % 16 == 4, "pad");
-  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && NB == 64, "ring");
+  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && (NB == 64 || NB == 32), "ring");
 };
 
-template <int NB, int K2, int RW, int RING, int BB>
-__global__ void __launch_bounds__(256, 1) bt2_apply_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols,
-                                                          int64_t n, const double* __restrict__ UV,
-                                                          const int64_t* __restrict__ gofs, int64_t nblk,
-                                                          long long* dbg) {
-  using C = BT2Cfg<NB, K2, RW, RING, BB>;
-  extern __shared__ __align__(128) double sh[];
-  double* Xs = sh;
-  double* G0 = Xs + C::XS;            // [2][U | V]
-  double* Zs = G0 + 2 * C::GS;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Zs + C::ZS);
-  long long ph[6] = {0, 0, 0, 0, 0, 0}, tprev = 0, nsteps = 0;
-  const bool prof = (dbg != nullptr) && blockIdx.x == 0 && threadIdx.x == 0;
-#define BT2_TS(k) do { if (prof) { long long _t = clock64(); ph[k] += _t - tprev; tprev = _t; } } while (0)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
-  const int64_t col0 = (int64_t)blockIdx.x * NB;
-  const int ncl = (int)smin<int64_t>(NB, ncols - col0);
-  const bool vec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-  if (nblk <= 0) return;
-  for (int e = tid; e < C::XS; e += 256) Xs[e] = 0.0;   // ring rows beyond n stay finite
-  if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_fence_init(); }
-  __syncthreads();
-
-  // Xs element (col, slot) lives at col*LDX + (slot ^ 4*bit2(col)): with LDX = 4 (mod 16) the
-  // GEMM1 B-fragment reads (8 columns x 4 slots) and the GEMM2 C read-modify-writes (4 column
-  // pairs x 8 slots) are both bank-conflict free.
-  auto xo = [&](int col, int slot) -> int { return col * C::LDX + (slot ^ (((col >> 2) & 1) << 2)); };
-  auto load_group = [&](int64_t g, int buf) {   // thread 0: one bulk copy of the [U | V] block
-    fence_proxy_async();
-    mbar_expect_tx(&bar[buf], (unsigned)(C::GS * sizeof(double)));
-    bulk_g2s(G0 + buf * C::GS, UV + g * C::GS, (unsigned)(C::GS * sizeof(double)), &bar[buf]);
-  };
-  // this thread's 2-row chunk of column cl: rows r0 + rr, rr = 2*lane (64-row blocks)
-  auto load_chunk = [&](int64_t r, int cl, int slot) {
-    double* dst = Xs + xo(cl, slot);
-    const double* src = X + SK_IDX(r, col0 + cl, ldx);
-    const int cnt = (cl < ncl) ? (int)smin<int64_t>(2, smax<int64_t>(0, n - r)) : 0;
-    if (vec) {
-      cp_async16(dst, cnt ? src : X, cnt * 8);
-    } else {
-      cp_async8(dst, cnt > 0 ? src : X, cnt > 0 ? 8 : 0);
-      cp_async8(dst + 1, cnt > 1 ? src + 1 : X, cnt > 1 ? 8 : 0);
-    }
-  };
-  auto load_rows64 = [&](int64_t r0, int slot0) {   // 64 rows x NB columns
-    const int rr = 2 * lane;
-    int slot = slot0 + rr;
-    if (slot >= RING) slot -= RING;
-#pragma unroll
-    for (int k = 0; k < NB / 8; k++) load_chunk(r0 + rr, warp + 8 * k, slot);
-  };
-  auto load_rows32 = [&](int64_t r0, int slot0) {   // 32 rows x NB columns
-    const int rr = 2 * (lane & 15);
-    int slot = slot0 + rr;
-    if (slot >= RING) slot -= RING;
-#pragma unroll
-    for (int k = 0; k < NB / 16; k++) load_chunk(r0 + rr, 2 * warp + (lane >> 4) + 16 * k, slot);
-  };
-  auto store_chunk = [&](int64_t r, int cl, int slot) {
-    if (cl >= ncl || r >= n) return;
-    double* dst = X + SK_IDX(r, col0 + cl, ldx);
-    const double2 v = *reinterpret_cast<const double2*>(Xs + xo(cl, slot));
-    if (vec && r + 1 < n) {
-      *reinterpret_cast<double2*>(dst) = v;
-    } else {
-      dst[0] = v.x;
-      if (r + 1 < n) dst[1] = v.y;
-    }
-  };
-  auto store_rows64 = [&](int64_t r0, int slot0) {
-    const int rr = 2 * lane;
-    int slot = slot0 + rr;
-    if (slot >= RING) slot -= RING;
-#pragma unroll
-    for (int k = 0; k < NB / 8; k++) store_chunk(r0 + rr, warp + 8 * k, slot);
-  };
-  auto store_rows32 = [&](int64_t r0, int slot0) {
-    const int rr = 2 * (lane & 15);
-    int slot = slot0 + rr;
-    if (slot >= RING) slot -= RING;
-#pragma unroll
-    for (int k = 0; k < NB / 16; k++) store_chunk(r0 + rr, 2 * warp + (lane >> 4) + 16 * k, slot);
-  };
-
-  unsigned phase[2] = {0u, 0u};
-  int buf = 0;
-  {
-    const int64_t blk = nblk - 1;
-    if (tid == 0) load_group(gofs[blk], 0);
-    load_rows64(blk * K2, 0);
-    load_rows32(blk * K2 + 64, 64);
-    cp_async_commit();
-  }
-  for (int64_t blk = nblk - 1; blk >= 0; blk--) {
-    const int64_t s0 = blk * K2;
-    const int64_t ntask = 1 + (n - 3 - s0) / BB;
-    for (int64_t t = 0; t < ntask; t++) {
-      const int64_t W0 = s0 + t * BB;
-      const int off = (int)((t * BB) % RING);
-      if (prof) { tprev = clock64(); nsteps++; }
-      cp_async_wait<0>();
-      mbar_wait(&bar[buf], phase[buf]);
-      phase[buf] ^= 1u;
-      __syncthreads();
-      BT2_TS(0);
-      // ---- prefetch the next group (and the next rows of the window, same block)
-      if (t + 1 < ntask) {
-        if (tid == 0) load_group(gofs[blk] + t + 1, buf ^ 1);
-        int so = off + RW;
-        if (so >= RING) so -= RING;
-        load_rows64(W0 + RW, so);
-      } else if (blk > 0) {
-        if (tid == 0) load_group(gofs[blk - 1], buf ^ 1);
-      }
-      cp_async_commit();
-      BT2_TS(1);
-      const double* Us = G0 + buf * C::GS;
-      const double* Vs = Us + K2 * C::LDW;
-      // ---- Z = U^T Xw : warps 2 (M: c fragments {h, h+2}, interleaved to balance U's zero
-      //      upper triangle) x 4 (N: NB/4 columns); even / odd k-step accumulator sets; next
-      //      fragments loaded before the current DMMAs.
-      {
-        constexpr int FN = NB / 32;          // 2 column fragments per warp
-        constexpr int NIT = RW / 8;
-        const int h = warp & 1, n0 = (warp >> 1) * (NB / 4);
-        double acc[2][2][FN][2];
-#pragma unroll
-        for (int p = 0; p < 2; p++)
-#pragma unroll
-          for (int i = 0; i < 2; i++)
-#pragma unroll
-            for (int j = 0; j < FN; j++) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
-        double fa[2][2][2], fb[2][FN][2];
-        auto ld1 = [&](int it, int sb) {
-          const int kk = it * 8;
-          int slot = off + kk;
-          if (slot >= RING) slot -= RING;
-#pragma unroll
-          for (int j = 0; j < FN; j++) {
-            fb[sb][j][0] = Xs[xo(n0 + 8 * j + gq, slot + tq)];
-            fb[sb][j][1] = Xs[xo(n0 + 8 * j + gq, slot + 4 + tq)];
-          }
-#pragma unroll
-          for (int i = 0; i < 2; i++) {
-            const int c = 8 * (h + 2 * i) + gq;
-            fa[sb][i][0] = Us[c * C::LDW + kk + tq];
-            fa[sb][i][1] = Us[c * C::LDW + kk + 4 + tq];
-          }
-        };
-        ld1(0, 0);
-#pragma unroll
-        for (int it = 0; it < NIT; it++) {
-          const int sb = it & 1;
-          if (it + 1 < NIT) ld1(it + 1, sb ^ 1);
-#pragma unroll
-          for (int i = 0; i < 2; i++) {
-            if (it * 8 + 7 < 8 * (h + 2 * i)) continue;   // U[rho][c] = 0 for rho <= c
-#pragma unroll
-            for (int j = 0; j < FN; j++) {
-              dmma884(acc[0][i][j][0], acc[0][i][j][1], fa[sb][i][0], fb[sb][j][0]);
-              dmma884(acc[1][i][j][0], acc[1][i][j][1], fa[sb][i][1], fb[sb][j][1]);
-            }
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 2; i++)
-#pragma unroll
-          for (int j = 0; j < FN; j++) {
-            const int c = 8 * (h + 2 * i) + gq, nn = n0 + 8 * j + 2 * tq;
-            Zs[nn * C::LDZ + c] = acc[0][i][j][0] + acc[1][i][j][0];
-            Zs[(nn + 1) * C::LDZ + c] = acc[0][i][j][1] + acc[1][i][j][1];
-          }
-      }
-      __syncthreads();
-      BT2_TS(2);
-      // ---- Xw -= V Z : M = RW (rho), N = NB, K = K2 (c); warps 4 (M, interleaved row
-      //      fragments: balanced staircase work) x 2 (N); zero staircase fragments skipped.
-      {
-        constexpr int FM = RW / 32, FN = NB / 16;
-        constexpr int NIT = K2 / 4;
-        const int wm = warp & 3, n0 = (warp >> 2) * (NB / 2);
-        double acc[FM][FN][2];
-#pragma unroll
-        for (int i = 0; i < FM; i++)
-#pragma unroll
-          for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-        double fa[2][FM], fb[2][FN];
-        auto ld2 = [&](int it, int sb) {
-          const int kk = it * 4;
-#pragma unroll
-          for (int j = 0; j < FN; j++) fb[sb][j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
-#pragma unroll
-          for (int i = 0; i < FM; i++) fa[sb][i] = Vs[(kk + tq) * C::LDW + 8 * (wm + 4 * i) + gq];
-        };
-        ld2(0, 0);
-#pragma unroll
-        for (int it = 0; it < NIT; it++) {
-          const int sb = it & 1, kk = it * 4;
-          if (it + 1 < NIT) ld2(it + 1, sb ^ 1);
-#pragma unroll
-          for (int i = 0; i < FM; i++) {
-            const int m0 = 8 * (wm + 4 * i);
-            if (m0 + 7 - kk < 1 || m0 - (kk + 3) > BB) continue;   // V[rho][c] != 0 iff 1 <= rho - c <= BB
-#pragma unroll
-            for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], fa[sb][i], fb[sb][j]);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < FM; i++) {
-          const int m0 = 8 * (wm + 4 * i);
-          int slot = off + m0;
-          if (slot >= RING) slot -= RING;
-#pragma unroll
-          for (int j = 0; j < FN; j++) {
-            int nn = n0 + 8 * j + 2 * tq;
-            Xs[xo(nn, slot + gq)] -= acc[i][j][0];
-            Xs[xo(nn + 1, slot + gq)] -= acc[i][j][1];
-          }
-        }
-      }
-      __syncthreads();
-      BT2_TS(3);
-      // ---- write back the rows leaving the window
-      if (t + 1 < ntask) {
-        store_rows64(W0, off);
-      } else {
-        store_rows64(W0, off);
-        store_rows32(W0 + 64, off + 64 >= RING ? off + 64 - RING : off + 64);
-        __syncthreads();
-        if (blk > 0) {
-          load_rows64((blk - 1) * K2, 0);   // first window of the next block
-          load_rows32((blk - 1) * K2 + 64, 64);
-        }
-        cp_async_commit();
-      }
-      BT2_TS(4);
-      buf ^= 1;
-    }
-  }
-  cp_async_wait<0>();
-  if (prof) {
-    for (int k = 0; k < 5; k++) dbg[k] = ph[k];
-    dbg[5] = nsteps;
-  }
-#undef BT2_TS
-}
-
-// Warp-specialised BT2 apply (the default): 8 consumer warps run only the two DMMA tiles per
-// step; a 9th producer warp moves the data one step ahead -- it waits until the consumers
+// Warp-specialised: 8 consumer warps run only the two DMMA tiles per step; 4 producer warps
+// move the data one step ahead -- it waits until the consumers
 // released step q-1 (mbarrier "empty"), writes that step's leaving rows back to X, then
 // loads step q+1's [U | V] block (one bulk TMA copy) and its new window rows (cp.async)
 // and signals mbarrier "full" (transaction bytes + cp.async completion arrivals).  The
@@ -1030,36 +783,54 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
   return cudaGetLastError();
 }
 
+static constexpr double kNB32Cost = 0.55;   // per-strip time of a 32-wide strip / a 64-wide one
+
 cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st) {
   if (L.n <= 2 || L.ngroups == 0 || ncols == 0) return cudaSuccess;
   cudaError_t e;
-  constexpr int NB = 64, K2 = 32, RW = 96, RING = 192, BB = 64;
+  constexpr int K2 = 32, RW = 96, RING = 192, BB = 64;
   if (L.k2 != K2 || L.b != BB) return cudaErrorInvalidValue;
   {
     KScope ks(KC_BT2_T, st);
     bt2_prep_kernel<K2, RW><<<(unsigned)std::min<int64_t>(L.ngroups, 8 * 148), 128, 0, st>>>(w.qv, w.qtau, L.ngroups,
                                                                                               BB, w.qT);
   }
-  using Cf = BT2Cfg<NB, K2, RW, RING, BB>;
-  e = cudaFuncSetAttribute(bt2_apply_kernel<NB, K2, RW, RING, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)Cf::SMEM);
-  if (e) return e;
   long long* dbgp = nullptr;
   if (getenv("SKEWEIG_BT2_DBG")) cudaMalloc(&dbgp, 6 * sizeof(long long));   // debug instrumentation only
-  const char* wsenv = getenv("SKEWEIG_BT2_WS");
-  const bool ws = !(wsenv && wsenv[0] == '0');
-  if (ws) {
-    const size_t smem = Cf::SMEM + 2 * sizeof(uint64_t);
-    e = cudaFuncSetAttribute(bt2_ws_kernel<NB, K2, RW, RING, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    KScope ks(KC_BT2, st);
-    bt2_ws_kernel<NB, K2, RW, RING, BB><<<(unsigned)((ncols + NB - 1) / NB), 384, smem, st>>>(
-        X, ldx, ncols, L.n, w.qT, w.gofs, L.nblk, dbgp);
-  } else {
-    KScope ks(KC_BT2, st);
-    bt2_apply_kernel<NB, K2, RW, RING, BB><<<(unsigned)((ncols + NB - 1) / NB), 256, Cf::SMEM, st>>>(
-        X, ldx, ncols, L.n, w.qT, w.gofs, L.nblk, dbgp);
+  // Column strips: 64 wide (best DMMA / smem ratio) and 32 wide (~0.55x the time of a
+  // 64-wide strip, measured: tools/bt2_time.py).  Every strip runs the whole step sequence,
+  // so the kernel time is (#waves) x (strip time); pick the mix of n64 wide and n32 narrow
+  // strips covering ncols with the fewest wave-units: e.g. one GPU, 32768 columns -> 444
+  // wide (3 full waves) + 136 narrow (one wave) instead of 3.46 -> 4 waves of wide strips;
+  // 8 ranks x 4096 columns -> 128 narrow strips (one wave) instead of 64 wide ones.
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t s64 = (ncols + 63) / 64;
+  int64_t n64 = s64;
+  double best = 1e300;
+  for (int64_t a64 = 0; a64 <= s64; a64++) {
+    const int64_t rest = std::max<int64_t>(0, ncols - 64 * a64);
+    const int64_t a32 = (rest + 31) / 32;
+    const double tw = (double)((a64 + nsm - 1) / nsm) + kNB32Cost * (double)((a32 + nsm - 1) / nsm);
+    if (tw < best - 1e-9) { best = tw; n64 = a64; }
   }
+  if (const char* v = getenv("SKEWEIG_BT2_NB")) n64 = (atoi(v) == 32) ? 0 : s64;   // experiments
+  const int64_t c64 = std::min<int64_t>(ncols, 64 * n64), c32 = ncols - c64;
+  auto launch = [&](auto kern, size_t smem, int NBv, int64_t cbeg, int64_t cnt) -> cudaError_t {
+    if (cnt <= 0) return cudaSuccess;
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2) return e2;
+    KScope ks(KC_BT2, st);
+    kern<<<(unsigned)((cnt + NBv - 1) / NBv), 384, smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk,
+                                                               dbgp);
+    return cudaGetLastError();
+  };
+  e = launch(bt2_ws_kernel<64, K2, RW, RING, BB>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64, 0, c64);
+  if (e) return e;
+  e = launch(bt2_ws_kernel<32, K2, RW, RING, BB>, BT2Cfg<32, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 32, c64,
+             c32);
+  if (e) return e;
   if (dbgp) {
     long long h[6];
     cudaMemcpyAsync(h, dbgp, sizeof(h), cudaMemcpyDeviceToHost, st);

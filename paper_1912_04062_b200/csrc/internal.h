@@ -152,7 +152,8 @@ struct B2TWork {
 
 struct TridWork {
   double* a2 = nullptr;        // alpha^2 (n)
-  double* lamc = nullptr;      // candidates (n)
+  double* lamc = nullptr;      // candidates (n + padding)
+  double* gtask = nullptr;     // Gershgorin bound per bisection task (n)
   int64_t* tsk = nullptr;      // 3 * n task arrays
   double* lamv = nullptr;      // per-vector perturbed lambda (nev)
   double* gblk = nullptr;      // per-vector block bound
@@ -198,7 +199,7 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
 // vectors of the global eigenpair range [k0, k1) (plus ghosts [vlo, k0)) go to Q columns 0..k1-vlo-1
 cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q, int64_t ldq,
                      TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st, int64_t k0, int64_t k1,
-                     int64_t* vlo_out);
+                     int64_t* vlo_out, const Dist* d = nullptr);
 cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st);
 // bt1.cu
 void bt1_reserve(Arena& ar, const F2BLayout& L, int64_t ncols, BT1Work& w);
