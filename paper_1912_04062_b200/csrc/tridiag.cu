@@ -33,7 +33,7 @@ __device__ __forceinline__ uint64_t td_splitmix64(uint64_t x) {
 // invariant as bisection: count(lo) <= i < count(hi)).  ~log_{K+1}(2g/tol) rounds instead of
 // log_2: the Sturm chain (one dependent division per row) is latency-bound, so K-fold more
 // counts per round cost little and the critical path shrinks ~3x for K = 8.  Same stopping
-// rule as the oracle's bisection (orc_bisect_one): width <= max(2 eps max|x|, eps g).
+// rule as plain bisection (reading of PAPER.md:616): width <= max(2 eps max|x|, eps g).
 // Sturm count on block [s0, s0+m): #{eigenvalues < sigma}
 __device__ __forceinline__ int td_sturm32(const double* __restrict__ a2, int64_t s0, int m, double sigma,
                                           double pivmin) {
