@@ -15,6 +15,8 @@
 #include "internal.h"
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 #include <nccl.h>
 
 namespace cg = cooperative_groups;
@@ -60,9 +62,8 @@ struct PanelArgs {
 };
 
 template <bool SMEM>
-__global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
+__device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double sm[];
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kb = a.kb;
   const int64_t rb = (int64_t)cta * a.R;
@@ -85,21 +86,28 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
     }
     __syncthreads();
   }
-  // partials for column k: rows gi > k: norm = sum x^2 (slot k), dots with columns c > k
+  // partials for column k: rows gi > k: norm = sum x^2 (slot k), dots with columns c > k.
+  // Thread (column k + tid%64, row group tid/64) sums every 4th row with two chains, then
+  // the 4 row groups are combined in fixed order (deterministic).
   auto partials = [&](int k) {
     const int buf = k & 1;
-    for (int c = k + warp; c < kb; c += 8) {
-      double s = 0.0;
-      for (int li = lane; li < nr; li += 32) {
-        int64_t gi = rb + li;
-        if (gi > k) s += P(li, k) * P(li, c);
-      }
-      s = warp_sum(s);
-      if (lane == 0) a.part[((size_t)buf * G + cta) * (kb + 1) + c] = s;
+    const int c = k + (tid & 63), rg = tid >> 6;
+    double s0 = 0.0, s1 = 0.0;
+    if (c < kb) {
+      int li = rg;
+      if (rb <= k) li += 4 * (int)((k - rb + 4 - rg) / 4);   // first li with rb + li > k, li = rg (mod 4)
+      for (; li + 4 < nr; li += 8) { s0 += P(li, k) * P(li, c); s1 += P(li + 4, k) * P(li + 4, c); }
+      if (li < nr) s0 += P(li, k) * P(li, c);
+    }
+    red[rg * (kb + 1) + (tid & 63)] = s0 + s1;
+    __syncthreads();
+    if (tid < 64 && k + tid < kb) {
+      const double t = (red[tid] + red[(kb + 1) + tid]) + (red[2 * (kb + 1) + tid] + red[3 * (kb + 1) + tid]);
+      a.part[((size_t)buf * G + cta) * (kb + 1) + k + tid] = t;
     }
     // owner of row k publishes row k (c >= k)
     if (k >= rb && k < re) {
-      for (int c = k + tid; c < kb; c += blockDim.x) a.rowk[buf * kb + c] = P((int)(k - rb), c);
+      for (int cc = k + tid; cc < kb; cc += blockDim.x) a.rowk[buf * kb + cc] = P((int)(k - rb), cc);
     }
   };
   partials(0);
@@ -257,6 +265,314 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
       a.T[r + c * a.ldt] = Ts[r * LDG + c];
     }
   }
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  panel_householder<SMEM>(a, sm);
+}
+
+// ------------------------------------------------------------------------------------
+// a1 + a2, default for tall panels: CholeskyQR2 + Householder reconstruction.  The
+// column-by-column Householder panel needs one grid-wide reduction per column (64 per
+// panel, latency-bound: ~0.6 ms per 32k-row panel, on the critical path of every rank in
+// the distributed reduction).  Here the panel costs seven grid barriers:
+//   P = Q1 R1, Q1 = P R1^-1 with R1^T R1 = P^T P (Cholesky), twice (CholQR2: Q orthonormal
+//   to working precision when kappa(P) <= ~1e7), then the compact WY form of the SAME
+//   orthogonal factor from Q (Ballard et al., "Reconstructing Householder vectors from
+//   tall-skinny QR"): Q - S = Y U (LU without pivoting, S = diag(-sign) of the running
+//   pivot, so |pivots| >= 1), V = Y (unit lower trapezoidal), T = -U S Y1^-T (upper), and
+//   I - V T V^T maps [I; 0] to Q S, i.e. P = (I - V T V^T) [S R; 0], R = R2 R1.
+// The result is a valid panel factorisation (PAPER.md:420-425 only needs an orthogonal
+// Q1^(j) = I - V T V^T with Q1^T P upper triangular); tau_i = T_ii.  When a Cholesky pivot
+// is <= 1e-12 max_i G_ii (kappa(P) >~ 1e6, e.g. rank-deficient panels) every CTA falls
+// back to the Householder panel above in the same launch (A is only written at the end).
+struct CqrArgs {
+  PanelArgs p;
+  double* scr;   // global scratch: [kb*kb] R1, [kb*kb] R (accumulated), [kb*kb] U, [kb] S, [2] flag
+  long long* dbg = nullptr;   // SKEWEIG_PANEL_DBG: phase clocks of CTAs 0 and 1
+};
+
+template <int KB>
+__global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  const PanelArgs& a = ca.p;
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t rb = (int64_t)cta * a.R;
+  const int nr = (int)smax<int64_t>(0, smin<int64_t>(a.m, rb + a.R) - rb);
+  const int LDP = (int)(a.R | 1);             // odd column stride of the panel rows in smem
+  constexpr int LDK = KB + 1;                 // odd leading dimension for kb x kb tiles
+  double* Ps = sm;                            // [KB][LDP]
+  double* Ms = sm + (size_t)KB * LDP;         // kb x LDK (R factor / U / T work)
+  double* Ms2 = Ms + KB * LDK;                // kb x LDK
+  double* aux = Ms2 + KB * LDK;               // [2 KB] diag inverses / signs
+  double* gR1 = ca.scr;
+  double* gR = gR1 + KB * KB;
+  double* gU = gR + KB * KB;
+  double* gS = gU + KB * KB;
+  double* gflag = gS + KB;
+  double* gfin = a.gram + (size_t)G * KB * KB;
+  auto P = [&](int li, int c) -> double& { return Ps[(size_t)c * LDP + li]; };
+  int nts = 0;
+  auto TS = [&]() { if (ca.dbg && cta < 2 && tid == 0 && nts < 16) ca.dbg[cta * 16 + nts++] = clock64(); };
+  TS();
+  for (int c = warp; c < KB; c += 8) {   // cp.async: every load in flight at once
+    const double* src = a.A + SK_IDX(rb, c, a.lda);
+    for (int li = lane; li < nr; li += 32) cp_async8(&Ps[(size_t)c * LDP + li], &src[li], 8);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  TS();
+  // Gram G = P^T P: thread (p, q) accumulates rows p + 16i, columns q + 16j (4 x 4), which
+  // keeps a half-warp's smem reads on distinct banks (odd LDP); fixed-order reduction over
+  // the CTAs, spread over every CTA (28 entries x 9 partial sums each, then combined in order)
+  auto gram = [&]() {
+    const int p = tid & 15, q = tid >> 4;
+    double g4[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) g4[i][j] = 0.0;
+#pragma unroll 2
+    for (int li = 0; li < nr; li++) {
+      double vr[4], vc[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) { vr[i] = P(li, p + 16 * i); vc[i] = P(li, q + 16 * i); }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) g4[i][j] += vr[i] * vc[j];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) a.gram[(size_t)cta * KB * KB + (p + 16 * i) + (q + 16 * j) * KB] = g4[i][j];
+    TS();
+    __threadfence();
+    grid.sync();
+    TS();
+    {
+      const int per = (KB * KB + G - 1) / G;   // entries of this CTA: [cta*per, cta*per + per)
+      const int le = tid / 9, part = tid % 9;
+      double* red9 = Ms2;                      // [28][9] partials (Ms2 is free here)
+      for (int base = 0; base < per; base += 28) {
+        const int e = cta * per + base + le;
+        double s = 0.0;
+        if (le < 28 && base + le < per && e < KB * KB)
+          for (int qq = part; qq < G; qq += 9) s += __ldcg(&a.gram[(size_t)qq * KB * KB + e]);
+        if (tid < 9 * 28) red9[tid] = s;
+        __syncthreads();
+        const int e2 = cta * per + base + tid;
+        if (tid < 28 && base + tid < per && e2 < KB * KB) {
+          double t = 0.0;
+          for (int k = 0; k < 9; k++) t += red9[tid * 9 + k];
+          gfin[e2] = t;
+        }
+        __syncthreads();
+      }
+    }
+    __threadfence();
+    grid.sync();
+    TS();
+  };
+  // CTA 0: kb x kb rank-1 trailing update Ms[r][c] -= x_r y_c over rows/cols > k (c >= r
+  // if upper): 16 x 16 threads, each a 4 x 4 register block, all loads before the stores
+  const int ti = tid >> 4, tj = tid & 15;
+  auto rank1 = [&](int k, const double* xrow, int xs, const double* yrow, bool upper) {
+    double xr[4], yc[4], m[4][4];
+    int rr[4], cc[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      rr[u] = k + 1 + ti + 16 * u;
+      cc[u] = k + 1 + tj + 16 * u;
+      xr[u] = xrow[(rr[u] < KB ? rr[u] : KB - 1) * xs];
+      yc[u] = yrow[cc[u] < KB ? cc[u] : KB - 1];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) m[u][v] = Ms[(rr[u] < KB ? rr[u] : KB - 1) * LDK + (cc[v] < KB ? cc[v] : KB - 1)];
+    __syncthreads();   // every read of row/column k and of the tile precedes the writes
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+      for (int v = 0; v < 4; v++)
+        if (rr[u] < KB && cc[v] < KB && (!upper || cc[v] >= rr[u])) Ms[rr[u] * LDK + cc[v]] = m[u][v] - xr[u] * yc[v];
+  };
+  // CTA 0: upper Cholesky G = R^T R in Ms (row-major r*LDK + c); returns ok
+  __shared__ int bad;
+  __shared__ double gmax;
+  auto cholesky = [&]() -> bool {
+    for (int e = tid; e < KB * KB; e += blockDim.x) Ms[(e % KB) * LDK + e / KB] = __ldcg(&gfin[e]);
+    __syncthreads();
+    if (warp == 0) {
+      double gm = fmax(Ms[lane * LDK + lane], Ms[(lane + 32) * LDK + lane + 32]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+      if (lane == 0) { gmax = gm; bad = 0; }
+    }
+    __syncthreads();
+    for (int k = 0; k < KB; k++) {
+      const double d = Ms[k * LDK + k];
+      const double rkk = (d > 0.0) ? sqrt(d) : 1.0, inv = 1.0 / rkk;
+      __syncthreads();
+      if (tid == 0 && !(d > 1e-12 * gmax)) bad = 1;
+      if (tid >= k && tid < KB) Ms[k * LDK + tid] = (tid == k) ? rkk : Ms[k * LDK + tid] * inv;
+      __syncthreads();
+      rank1(k, Ms + k * LDK, 1, Ms + k * LDK, true);   // x_r = R[k][r], y_c = R[k][c]
+      __syncthreads();
+    }
+    for (int e = tid; e < KB * KB; e += blockDim.x) {
+      const int r = e / KB, c = e % KB;
+      if (c < r) Ms[r * LDK + c] = 0.0;
+    }
+    __syncthreads();
+    return bad == 0;
+  };
+  // row li of P <- (row li of P) Rm^-1, Rm upper (row-major, LDK) with inverse diagonal
+  // dinv: 16-column register blocks, left-looking over the finished blocks (in smem)
+  auto solve_row = [&](int li, const double* Rm, const double* dinv) {
+#pragma unroll 1
+    for (int cb = 0; cb < KB; cb += 16) {
+      double x[16];
+#pragma unroll
+      for (int c = 0; c < 16; c++) x[c] = P(li, cb + c);
+#pragma unroll 4
+      for (int j = 0; j < cb; j++) {
+        const double xj = P(li, j);
+#pragma unroll
+        for (int c = 0; c < 16; c++) x[c] -= xj * Rm[j * LDK + cb + c];
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        x[j] *= dinv[cb + j];
+#pragma unroll
+        for (int c = j + 1; c < 16; c++) x[c] -= x[j] * Rm[(cb + j) * LDK + cb + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 16; c++) P(li, cb + c) = x[c];
+    }
+  };
+  // every CTA: rows of P <- P R^-1 with R (upper) from global, right-looking per row
+  auto trsm_rows = [&](const double* gRm) {
+    for (int e = tid; e < KB * KB; e += blockDim.x) Ms2[(e / KB) * LDK + e % KB] = __ldcg(&gRm[e]);   // row-major
+    __syncthreads();
+    if (tid < KB) aux[tid] = 1.0 / Ms2[tid * LDK + tid];
+    __syncthreads();
+    for (int li = tid; li < nr; li += blockDim.x) solve_row(li, Ms2, aux);
+    __syncthreads();
+  };
+  bool ok = true;
+  for (int pass = 0; pass < 2 && ok; pass++) {
+    gram();
+    if (cta == 0) {
+      const bool okc = cholesky();
+      // R (row-major) -> global; pass 0: R1; pass 1: R = R2 R1
+      if (pass == 0) {
+        for (int e = tid; e < KB * KB; e += blockDim.x) gR1[e] = Ms[(e / KB) * LDK + e % KB];
+      } else {
+        for (int e = tid; e < KB * KB; e += blockDim.x) Ms2[(e / KB) * LDK + e % KB] = __ldcg(&gR[e]);   // R1
+        __syncthreads();
+        for (int e = tid; e < KB * KB; e += blockDim.x) {
+          const int r = e / KB, c = e % KB;
+          double s = 0.0;
+          for (int l = r; l <= c; l++) s += Ms[r * LDK + l] * Ms2[l * LDK + c];
+          gR1[e] = Ms[r * LDK + c];        // R2 (for the solve)
+          gR[e] = s;                       // R2 R1
+        }
+      }
+      if (pass == 0)
+        for (int e = tid; e < KB * KB; e += blockDim.x) gR[e] = Ms[(e / KB) * LDK + e % KB];
+      if (tid == 0) gflag[0] = okc ? 0.0 : 1.0;
+    }
+    TS();
+    __threadfence();
+    grid.sync();
+    ok = __ldcg(&gflag[0]) == 0.0;
+    if (ok) trsm_rows(gR1);
+    TS();
+  }
+  if (!ok) {   // ill-conditioned or rank-deficient panel: Householder, same launch
+    __syncthreads();
+    panel_householder<true>(a, sm);
+    return;
+  }
+  // ---- Householder reconstruction: CTA 0 holds rows 0..kb-1 (R >= kb)
+  if (cta == 0) {
+    // modified LU of Q1 - S (Q1 = top kb x kb of Q) in Ms (row-major)
+    for (int e = tid; e < KB * KB; e += blockDim.x) Ms[(e / KB) * LDK + e % KB] = P(e / KB, e % KB);
+    __syncthreads();
+    for (int k = 0; k < KB; k++) {
+      const double d = Ms[k * LDK + k];
+      const double sg = (d >= 0.0) ? -1.0 : 1.0;   // S_kk = -sign(d): pivot d - S_kk, |.| >= 1
+      const double piv = d - sg, inv = 1.0 / piv;
+      __syncthreads();
+      if (tid == 0) { aux[k] = sg; Ms[k * LDK + k] = piv; }
+      if (tid > k && tid < KB) Ms[tid * LDK + k] *= inv;   // L column
+      __syncthreads();
+      rank1(k, Ms + k, LDK, Ms + k * LDK, false);   // x_r = L[r][k], y_c = U[k][c]
+      __syncthreads();
+    }
+    for (int e = tid; e < KB * KB; e += blockDim.x) {
+      const int r = e / KB, c = e % KB;
+      gU[e] = (c >= r) ? Ms[r * LDK + c] : 0.0;   // U row-major
+    }
+    if (tid < KB) gS[tid] = aux[tid];
+  }
+  TS();
+  __threadfence();
+  grid.sync();
+  TS();
+  // V: rows >= kb: y = q U^-1 (row solve with U upper, right-looking); rows < kb: L1
+  for (int e = tid; e < KB * KB; e += blockDim.x) Ms2[(e / KB) * LDK + e % KB] = __ldcg(&gU[e]);
+  __syncthreads();
+  if (tid < KB) aux[KB + tid] = 1.0 / Ms2[tid * LDK + tid];
+  __syncthreads();
+  for (int li = tid; li < nr; li += blockDim.x) {
+    const int64_t gi = rb + li;
+    if (gi >= KB) {
+      solve_row(li, Ms2, aux + KB);
+      for (int c = 0; c < KB; c++) a.V[SK_IDX(gi, c, a.ldv)] = P(li, c);
+    } else {   // CTA 0: L1 (unit lower)
+      for (int c = 0; c < KB; c++) a.V[SK_IDX(gi, c, a.ldv)] = (c < gi) ? Ms[gi * LDK + c] : (c == gi ? 1.0 : 0.0);
+    }
+  }
+  if (cta == 0) {
+    // T = -U S Y1^-T (row r: t L1^T = -(U S)_r, forward over c), tau = diag(T); R_h = S R -> A
+    __syncthreads();
+    double* Ts = Ms2;   // overwrite U copy (no longer needed by CTA 0 after the V rows)
+    double* ws = Ps;    // the panel rows are no longer needed either
+    for (int e = tid; e < KB * KB; e += blockDim.x) {
+      const int r = e / KB, c = e % KB;
+      ws[r * LDK + c] = (c >= r) ? -__ldcg(&gU[e]) * aux[c] : 0.0;
+    }
+    __syncthreads();
+    // T Y1^T = W column by column: T[:, c] = W[:, c] - sum_{l<c} T[:, l] Y1[c][l]; thread
+    // (row r, quarter q) sums l = q, q+4, ..; the 4 quarters combine with shuffles
+    {
+      const int r = tid >> 2, q = tid & 3;
+      for (int c = 0; c < KB; c++) {
+        double t = 0.0;
+        for (int l = r + q; l < c; l += 4) t += Ts[r * LDK + l] * Ms[c * LDK + l];
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        if (q == 0) Ts[r * LDK + c] = (c < r) ? 0.0 : ws[r * LDK + c] - t;
+        __syncthreads();
+      }
+    }
+    for (int e = tid; e < KB * KB; e += blockDim.x) {
+      const int r = e % KB, c = e / KB;
+      a.T[r + c * a.ldt] = Ts[r * LDK + c];
+      if (r <= c) a.A[SK_IDX(r, c, a.lda)] = aux[r] * __ldcg(&gR[r * KB + c]);
+      else a.A[SK_IDX(r, c, a.lda)] = 0.0;
+    }
+    if (tid < KB) a.tau[tid] = Ts[tid * LDK + tid];
+  }
+  __syncthreads();
+  TS();
 }
 
 // ------------------------------------------------------------------------------------
@@ -527,11 +843,13 @@ void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w, int P) {
   w.Q = ar.take<double>(ldn * 2 * b);
   w.zpart = ar.take<double>(((n + kWRows - 1) / kWRows + 2) * b * b);
   w.Mb = ar.take<double>(b * b);
+  w.cqr = ar.take<double>(3 * (size_t)b * b + b + 2);
   if (P > 1) w.Ycol = ar.take<double>((size_t)P * ldn * b);
 }
 
 static int panel_grid(int64_t m, int nsm) {
   int64_t g = (m + 63) / 64;   // at least 64 rows per CTA
+  if (const char* v = getenv("SKEWEIG_PANEL_G")) nsm = std::max(1, std::min(nsm, atoi(v)));   // experiments
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, nsm));
 }
 
@@ -557,6 +875,43 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   void* args[] = {&a};
   cudaError_t e;
   KScope ks(KC_PANEL, st);
+  // CholeskyQR2 + reconstruction when CTA 0 holds the top b rows and the rows fit in smem
+  const size_t cqr_smem = ((size_t)b * (a.R | 1) + 2 * (size_t)b * (b + 1) + 2 * b + 4) * sizeof(double);
+  const char* hh = getenv("SKEWEIG_PANEL_HH");   // experiments: force the Householder panel
+  if (b == 64 && a.R >= b && cqr_smem <= 200 * 1024 && !(hh && hh[0] == '1')) {
+    static bool set = false;
+    if (!set) {
+      e = cudaFuncSetAttribute(panel_cqr_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + (int)extra);
+      if (e) return e;
+      set = true;
+    }
+    CqrArgs ca;
+    ca.p = a;
+    ca.scr = w.cqr;
+    static long long* dbgp = nullptr;
+    if (getenv("SKEWEIG_PANEL_DBG") && j == 3) {
+      if (!dbgp) cudaMalloc(&dbgp, 32 * sizeof(long long));
+      ca.dbg = dbgp;
+    }
+    void* cargs[] = {&ca};
+    const size_t sm_c = std::max(cqr_smem, smem_full);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, panel_cqr_kernel<64>, 256, sm_c);
+    if (occ * nsm >= G) {
+      e = cudaLaunchCooperativeKernel((void*)panel_cqr_kernel<64>, dim3(G), dim3(256), cargs, sm_c, st);
+      if (ca.dbg) {
+        long long h[32];
+        cudaMemcpyAsync(h, ca.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        for (int c = 0; c < 2; c++) {
+          fprintf(stderr, "[cqr cta%d]", c);
+          for (int i = 1; i < 16 && h[c * 16 + i] > h[c * 16]; i++) fprintf(stderr, " %lld", h[c * 16 + i] - h[c * 16 + i - 1]);
+          fprintf(stderr, "\n");
+        }
+      }
+      return e;
+    }
+  }
   if (use_smem) {
     static bool set = false;
     if (!set) {

@@ -130,6 +130,7 @@ struct F2BWork {
   double* Q = nullptr;       // n x 2b
   double* zpart = nullptr;   // V^T X partials
   double* Mb = nullptr;      // b x b
+  double* cqr = nullptr;     // CholeskyQR panel scratch (3 b^2 + b + 2)
   double* Ycol = nullptr;    // distributed skew-SYMM column-part pieces (P x n x b)
 };
 
