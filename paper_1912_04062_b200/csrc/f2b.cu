@@ -876,9 +876,14 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   cudaError_t e;
   KScope ks(KC_PANEL, st);
   // CholeskyQR2 + reconstruction when CTA 0 holds the top b rows and the rows fit in smem
-  const size_t cqr_smem = ((size_t)b * (a.R | 1) + 2 * (size_t)b * (b + 1) + 2 * b + 4) * sizeof(double);
+  // (its own grid: floor(m/b) CTAs at most, so that every CTA -- CTA 0 in particular --
+  // holds >= b rows)
+  const int Gc = (int)std::max<int64_t>(1, std::min<int64_t>(m / b, nsm));
+  const int64_t Rc = (m + Gc - 1) / Gc;
+  const size_t cqr_smem = ((size_t)b * (Rc | 1) + 2 * (size_t)b * (b + 1) + 2 * b + 4) * sizeof(double);
   const char* hh = getenv("SKEWEIG_PANEL_HH");   // experiments: force the Householder panel
-  if (b == 64 && a.R >= b && cqr_smem <= 200 * 1024 && !(hh && hh[0] == '1')) {
+  if (b == 64 && m >= b && Rc >= b && cqr_smem <= 200 * 1024 && (size_t)b * Rc * sizeof(double) + extra <= 200 * 1024 &&
+      !(hh && hh[0] == '1')) {
     static bool set = false;
     if (!set) {
       e = cudaFuncSetAttribute(panel_cqr_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + (int)extra);
@@ -887,6 +892,8 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
     }
     CqrArgs ca;
     ca.p = a;
+    ca.p.R = Rc;
+    ca.p.smem_rows = (int)Rc;
     ca.scr = w.cqr;
     static long long* dbgp = nullptr;
     if (getenv("SKEWEIG_PANEL_DBG") && j == 3) {
@@ -894,11 +901,12 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
       ca.dbg = dbgp;
     }
     void* cargs[] = {&ca};
-    const size_t sm_c = std::max(cqr_smem, smem_full);
+    // smem: the CholQR layout, or the Householder fallback's (same grid, Rc rows per CTA)
+    const size_t sm_c = std::max(cqr_smem, std::max((size_t)b * Rc * sizeof(double), tbuild) + extra);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, panel_cqr_kernel<64>, 256, sm_c);
-    if (occ * nsm >= G) {
-      e = cudaLaunchCooperativeKernel((void*)panel_cqr_kernel<64>, dim3(G), dim3(256), cargs, sm_c, st);
+    if (occ * nsm >= Gc) {
+      e = cudaLaunchCooperativeKernel((void*)panel_cqr_kernel<64>, dim3(Gc), dim3(256), cargs, sm_c, st);
       if (ca.dbg) {
         long long h[32];
         cudaMemcpyAsync(h, ca.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
