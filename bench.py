@@ -243,8 +243,9 @@ def run_ours(args):
     value = fm["total"] / (ms_step * 1e-3) / 1e12
     launches = sum(v[1] for v in kstats.values())
     # dominant kernel roofline (FP64 DMMA contraction)
-    hot = {"bt2_apply": fm["bt2_apply"] * (k1 - k0) / nev, "skew_r2k": fm["skew_r2k"],
-           "skew_symm": fm["skew_symm"], "bt1_update": fm["bt1"] / 2 * (k1 - k0) / nev,
+    # per-rank shares: eigenvector columns (k1-k0)/nev; F2B trailing work ~1/ws (block-cyclic columns)
+    hot = {"bt2_apply": fm["bt2_apply"] * (k1 - k0) / nev, "skew_r2k": fm["skew_r2k"] / ws,
+           "skew_symm": fm["skew_symm"] / ws, "bt1_update": fm["bt1"] / 2 * (k1 - k0) / nev,
            "bt1_z": fm["bt1"] / 2 * (k1 - k0) / nev}
     dom = max(hot, key=lambda k: kstats.get(k, [0, 0])[0])
     dms, dla = kstats[dom]

@@ -83,7 +83,6 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(ChaseArgs a) {
     const int ntprev = (s > 0) ? (int)chase_ntask(n, b, s - 1) : 0;
     const int64_t gbase = a.gofs[s / a.k2];
     const int cpos = (int)(s % a.k2);
-    volatile int* prme = a.progress + s;
     // task geometry: left column col, reflector rows [r, r+L), block rows [c, e)
     auto geom = [&](int t, int64_t& col, int64_t& r, int& L) {
       if (t == 0) { col = s; r = s + 1; L = (int)smin<int64_t>(b, n - 1 - s); }
@@ -138,9 +137,8 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(ChaseArgs a) {
         // ---- (1) dependency: sweep s-1 tasks 0..t+1 complete (warp 0 polls, whole warp)
         if (warp == 0 && s > 0) {
           const int need = min(t + 2, ntprev);
-          volatile int* pr = a.progress + (s - 1);
-          while (*pr < need) { }
-          __threadfence();
+          const int* pr = a.progress + (s - 1);
+          while (ld_acquire_gpu(pr) < need) { }
         }
         named_bar(1, NCT);
         if (prof) { long long now = clock64(); t_wait += now - tk; tk = now; tp = now; ntasks++; }
@@ -172,6 +170,8 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(ChaseArgs a) {
         //      thread pair (every other j), four independent chains, branch-free bodies
         const int part = tid / (3 * MAXB), it = tid % (3 * MAXB);
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        // dbase[j] computed in registers (no dependent shared load in the chains)
+        auto colb = [&](int j) -> int { int x = sr0 + j; x = (x >= B2) ? x - B2 : x; return x * LDW - j; };
         auto dot4 = [&](auto&& f) {
           int j = part;
           for (; j + 6 < L; j += 8) { acc0 += f(j); acc1 += f(j + 2); acc2 += f(j + 4); acc3 += f(j + 6); }
@@ -192,12 +192,12 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(ChaseArgs a) {
             // stride LDW-1; j == i reads the stored zero diagonal
             dot4([&](int j) {
               const bool lo = j < i;
-              return W[lo ? dbase[j] + i : si + j] * (lo ? vs[j] : -vs[j]);
+              return W[lo ? colb(j) + i : si + j] * (lo ? vs[j] : -vs[j]);
             });
           }
         } else if (it < 3 * b) {
           const int i = it - 2 * b;
-          if (i < ne) dot4([&](int j) { return W[dbase[j] + L + i] * vs[j]; });
+          if (i < ne) dot4([&](int j) { return W[colb(j) + L + i] * vs[j]; });
         }
         if (it < 3 * b) red[part][it] = (acc0 + acc1) + (acc2 + acc3);
         named_bar(1, NCT);
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(ChaseArgs a) {
       if (warp == kChaseCW) {
         // ---- auxiliary warp: task t complete (all its writes precede the barrier, incl. the
         //      beta of task t+1), then the next task's final left column and reflector
-        if (lane == 0) { __threadfence(); *prme = t + 1; }
+        if (lane == 0) st_release_gpu(a.progress + s, t + 1);   // after the CTA barrier: cumulative
         if (!last) { __syncwarp(); store_col_refl(t + 1); }
       }
       C2_TS(3);
