@@ -597,6 +597,7 @@ struct SymmArgs {
   int P = 1, qoff = 0;
   int64_t nt = 0, nloc = 0;
   double* Ycol = nullptr; int64_t ldy = 0;
+  int split = 1;   // single device: > 1 = split-K pieces per row block (Ycol[0..split))
 };
 
 template <int BM, int NB, int BK, int STAGES>
@@ -607,7 +608,8 @@ struct SymmParts {
   using Acc = double[TR::FM][TR::FN][2];
 
   // acc += sum over local column blocks q <= p of L_pq U_q   (diagonal block strictly lower)
-  __device__ static void row_part(const SymmArgs& s, double* smem, int64_t p, Acc& acc) {
+  __device__ static void row_part(const SymmArgs& s, double* smem, int64_t p, Acc& acc, int64_t ks0 = 0,
+                                  int64_t ks1 = INT64_MAX) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm0 = (warp % TR::NWARP_M) * 32, wn0 = (warp / TR::NWARP_M) * 32;
     const int64_t m0 = p * BM;
@@ -619,9 +621,9 @@ struct SymmParts {
     constexpr int KPB = BM / BK;   // k-steps per column block
     const int qoff = s.qoff, P = s.P;
     const int64_t nq = (p >= qoff) ? (p - qoff) / P + 1 : 0;
-    const int64_t nk = nq * KPB;
-    auto kofs = [&](int64_t kb64) -> int64_t {   // local k-step -> global column offset (32-bit math)
-      const int kb = (int)kb64;
+    const int64_t kbeg = smin<int64_t>(ks0, nq * KPB), nk = smin<int64_t>(ks1, nq * KPB) - kbeg;   // k-steps
+    auto kofs = [&](int64_t j64) -> int64_t {   // k-step kbeg+j -> global column offset (32-bit math)
+      const int kb = (int)(kbeg + j64);
       return (int64_t)((qoff + P * (kb / KPB)) * BM + (kb % KPB) * BK);
     };
     for (int st = 0; st < STAGES - 1; st++) {
@@ -725,7 +727,27 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
 #pragma unroll
     for (int j = 0; j < TR::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int64_t bid = blockIdx.x;
-  if (s.P == 1) {
+  if (s.split > 1) {
+    // single device, split-K: row block p, piece k of its "virtual" K range -- the row part
+    // (k-steps of the column blocks 0..p) followed by the column part (rows p*BM .. m) --
+    // into Ycol[k]; a combine kernel sums the pieces.  Equal-size CTAs, no long tail.
+    const int64_t p = bid / s.split, k = bid % s.split;
+    constexpr int KPB = BM / BK;
+    const int64_t kr = (p + 1) * KPB;                             // row-part k-steps
+    const int64_t kc = (s.m - p * BM + BK - 1) / BK;              // column-part k-steps
+    const int64_t kv = kr + kc;
+    const int64_t v0 = (kv * k) / s.split, v1 = (kv * (k + 1)) / s.split;
+    if (v0 < kr) SP::row_part(s, smem, p, acc, v0, smin<int64_t>(v1, kr));
+#pragma unroll
+    for (int i = 0; i < TR::FM; i++)
+#pragma unroll
+      for (int j = 0; j < TR::FN; j++) { acc[i][j][0] = -acc[i][j][0]; acc[i][j][1] = -acc[i][j][1]; }
+    if (v1 > kr) {
+      const int64_t r0 = p * BM + (smax<int64_t>(v0, kr) - kr) * BK, r1 = smin<int64_t>(s.m, p * BM + (v1 - kr) * BK);
+      SP::col_part(s, smem, p, r0, r1, acc);
+    }
+    SP::store(s, s.Ycol + (size_t)k * s.ldy * s.nb, s.ldy, p * BM, -1.0, acc);
+  } else if (s.P == 1) {
     SP::row_part(s, smem, bid, acc);
 #pragma unroll
     for (int i = 0; i < TR::FM; i++)
@@ -743,6 +765,16 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
     const int64_t b0 = c + (nrb * k) / s.P, b1 = c + (nrb * (k + 1)) / s.P;
     SP::col_part(s, smem, c, b0 * BM, smin<int64_t>(s.m, b1 * BM), acc);
     SP::store(s, s.Ycol + (size_t)k * s.ldy * s.nb, s.ldy, c * BM, 1.0, acc);
+  }
+}
+
+// X = sum_k Ycol[k] (single-device split-K skew-SYMM; fixed order)
+__global__ void symm_sum_kernel(double* X, int64_t ldx, const double* Ycol, int64_t ldy, int npieces, int64_t m) {
+  const int64_t col = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < npieces; k++) s += Ycol[(size_t)k * ldy * gridDim.y + i + col * ldy];
+    X[i + col * ldx] = s;
   }
 }
 
@@ -826,6 +858,7 @@ __global__ void pq_build_kernel(const double* V, int64_t ldv, int64_t m, int kb,
 // Host driver.
 
 static constexpr int kSymmBM = 64, kSymmBK = 16, kSymmStages = 2;
+static constexpr int kSymmMaxSplit = 6, kSymmNsm = 148;
 static constexpr int kWRows = 256;
 
 void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w, int P) {
@@ -844,7 +877,7 @@ void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w, int P) {
   w.zpart = ar.take<double>(((n + kWRows - 1) / kWRows + 2) * b * b);
   w.Mb = ar.take<double>(b * b);
   w.cqr = ar.take<double>(3 * (size_t)b * b + b + 2);
-  if (P > 1) w.Ycol = ar.take<double>((size_t)P * ldn * b);
+  w.Ycol = ar.take<double>((size_t)std::max(P, kSymmMaxSplit) * ldn * b);
 }
 
 static int panel_grid(int64_t m, int nsm) {
@@ -975,17 +1008,35 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     }
     const int64_t nt = (m + kSymmBM - 1) / kSymmBM;
     int64_t grid = nt;
+    int split = 1;
+    if (d.P == 1) {
+      // split-K pieces per row block: minimise (max CTAs per SM) x (work per CTA) + combine
+      double best = 1e300;
+      for (int c = 1; c <= kSymmMaxSplit; c++) {
+        const double t = (double)((nt * c + kSymmNsm - 1) / kSymmNsm) / c + 0.02 * (c > 1 ? c : 0);
+        if (t < best - 1e-12) { best = t; split = c; }
+      }
+      if (const char* v = getenv("SKEWEIG_SYMM_SPLIT")) split = std::max(1, std::min(kSymmMaxSplit, atoi(v)));   // experiments
+      if (split > 1) {
+        s.split = split;
+        s.Ycol = w.Ycol; s.ldy = ldn;
+        grid = nt * split;
+      }
+    }
     if (d.P > 1) {
       s.nt = nt;
       s.nloc = (nt > qoff) ? (nt - qoff + d.P - 1) / d.P : 0;
       s.Ycol = w.Ycol; s.ldy = ldn;
       grid = nt + (int64_t)d.P * s.nloc;
     }
-    KScope ks(KC_SYMM, st, d.P > 1 ? 2 : 1);
+    KScope ks(KC_SYMM, st, (d.P > 1 || split > 1) ? 2 : 1);
     symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages><<<(unsigned)grid, TR::NTHREADS, smem, st>>>(s);
     if (d.P > 1) {
       dim3 cg((unsigned)std::min<int64_t>((m + 255) / 256, 64), (unsigned)b);
       symm_combine_kernel<<<cg, 256, 0, st>>>(Wp, ldn, w.Ycol, ldn, d.P, m, b, kSymmBM, d.P, qoff);
+    } else if (split > 1) {
+      dim3 cg((unsigned)std::min<int64_t>((m + 255) / 256, 64), (unsigned)b);
+      symm_sum_kernel<<<cg, 256, 0, st>>>(Wp, ldn, w.Ycol, ldn, split, m);
     }
   }
   if (d.P > 1) {   // Y = sum over ranks of the partial skew-SYMM products (NVLink allreduce)
