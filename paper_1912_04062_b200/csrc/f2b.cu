@@ -830,16 +830,22 @@ __global__ void zsum_kernel(const double* part, int nchunk, int cnt, double* Z) 
   for (int q = 0; q < nchunk; q++) s += part[(size_t)q * cnt + e];
   Z[e] = s;
 }
-// (3) Mb = T^T Z (kb x kb, T upper), one CTA
+// (3) Mb = T^T Z (kb x kb, T upper): CTA c forms column c, thread a the element (a, c);
+// T staged in shared memory (column a contiguous per thread: odd stride, conflict-free)
 __global__ void mb_kernel(const double* Z, const double* T, int ldt, int kb, double* Mb) {
-  extern __shared__ double zs[];   // kb x kb (T is read through L1/L2)
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) zs[e] = Z[e];
-  __syncthreads();
+  extern __shared__ double ts[];   // kb x (kb + 1): ts[a * (kb+1) + l] = T[l, a]
+  double* zc = ts + kb * (kb + 1);
+  const int c = blockIdx.x;
   for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    const int a = e % kb, c = e / kb;
+    const int l = e % kb, a = e / kb;
+    ts[a * (kb + 1) + l] = T[l + (size_t)a * ldt];
+  }
+  for (int l = threadIdx.x; l < kb; l += blockDim.x) zc[l] = Z[l + (size_t)c * kb];
+  __syncthreads();
+  for (int a = threadIdx.x; a < kb; a += blockDim.x) {
     double s = 0.0;
-    for (int l = 0; l <= a; l++) s += T[l + a * ldt] * zs[l + c * kb];   // (T^T)_{a l} = T_{l a}
-    Mb[e] = s;
+    for (int l = 0; l <= a; l++) s += ts[a * (kb + 1) + l] * zc[l];   // (T^T)_{a l} = T_{l a}
+    Mb[a + (size_t)c * kb] = s;
   }
 }
 // (4) P = [V W], Q = [W -V] with W already in P[:, kb:2kb]
@@ -1050,7 +1056,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     vtx_partial_kernel<16><<<nchunk, 128, TV::SMEM_BYTES, st>>>(Vj, ldv, Wp, ldn, m, kWRows, w.zpart);
     double* Zr = w.zpart + (size_t)nchunk * b * b;
     zsum_kernel<<<(b * b + 255) / 256, 256, 0, st>>>(w.zpart, nchunk, b * b, Zr);
-    mb_kernel<<<1, 256, b * b * sizeof(double), st>>>(Zr, Tj, b, b, w.Mb);
+    mb_kernel<<<b, 64, (size_t)(b * (b + 1) + b) * sizeof(double), st>>>(Zr, Tj, b, b, w.Mb);
     GemmArgs ga;
     ga.M = m; ga.N = b; ga.K = b;
     ga.A = Vj; ga.lda = ldv; ga.B = w.Mb; ga.ldb = b; ga.C = Wp; ga.ldc = ldn; ga.alpha = -0.5; ga.beta = 1.0;

@@ -165,6 +165,8 @@ struct TridWork {
   double* part = nullptr;      // gram partials
   double* H = nullptr;         // projection coefficients
   double* Rinv = nullptr;
+  double* rpart = nullptr;     // fused reorthogonalisation: per-CTA Gram partials + reduced H
+  int64_t* rblk = nullptr;     // fused reorthogonalisation: per 32-vector block (k0, p0, nb)
   int64_t batch = 0;
 };
 

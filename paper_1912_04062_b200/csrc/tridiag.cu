@@ -17,8 +17,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cfloat>
+#include <cooperative_groups.h>
 
 namespace sk {
+
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ uint64_t td_splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -407,6 +410,214 @@ __global__ void assemble_D_kernel(const double* Q, int64_t ldq, int64_t n, int64
 }
 
 // ------------------------------------------------------------------------------------
+// Fused block re-orthogonalisation (reading R9(4)): one cooperative launch for all 32-vector
+// blocks.  CTA c owns the rows [c R, (c+1) R) of every vector, so a block only depends on
+// rows this CTA wrote for the earlier blocks; grid barriers are needed only around the
+// cross-CTA reductions of the Gram matrices (8 per block: 2 per CGS pass, 2 per CholQR pass).
+// The row slices are staged column-major in shared memory (LD = 4 mod 16: conflict-free
+// DMMA fragments for both A = X^T and A = X); all products run on DMMA m8n8k4.
+static constexpr int kReorthMaxG = 160;   // >= co-resident CTAs (1 per SM)
+static constexpr int kRfCnt = 64 * 32;    // Gram partial: 64 (previous) x 32 (block)
+static constexpr int kRfHLD = 36;         // H / R^-1 row stride (4 mod 16)
+
+struct ReorthArgs {
+  double* Q; int64_t ldq; int64_t n;
+  const int64_t* blk; int nblk;   // per block: k0, p0, nb (columns relative to Q)
+  double* part;                    // G x kRfCnt partials, then kRfCnt reduced
+  int R, LDR;                      // rows per CTA (multiple of 8), smem column stride
+};
+
+// partial Gram: out(i, j) = sum_r X(r, i) Y(r, j), i < 8*FI (X columns), j < 32; X, Y column-major
+// in smem (LDR); warp w takes fragment row fi = w % FI_TOTAL groups.
+__device__ __forceinline__ void rf_gram(const double* Xs, const double* Ys, int LDR, int R, int fi_cnt, int sym,
+                                        double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t = lane & 3;
+  if (!sym) {   // fi_cnt x 4 fragments: warp w -> fragment row w, all 4 column fragments
+    if (warp < fi_cnt) {
+      double acc[4][2] = {};
+      const double* xa = Xs + (8 * warp + gq) * LDR + t;
+      for (int k = 0; k < R; k += 4) {
+        const double a = xa[k];
+#pragma unroll
+        for (int f = 0; f < 4; f++) dmma884(acc[f][0], acc[f][1], a, Ys[(8 * f + gq) * LDR + k + t]);
+      }
+#pragma unroll
+      for (int f = 0; f < 4; f++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) out[(8 * warp + gq) + 64 * (8 * f + 2 * t + h)] = acc[f][h];
+    }
+  } else {      // 4 x 4 fragments of Y^T Y: warp w -> row fragment w & 3, column fragments 2 (w >> 2) + {0, 1}
+    const int fi = warp & 3, fj0 = 2 * (warp >> 2);
+    double acc[2][2] = {};
+    const double* xa = Xs + (8 * fi + gq) * LDR + t;
+    for (int k = 0; k < R; k += 4) {
+      const double a = xa[k];
+#pragma unroll
+      for (int f = 0; f < 2; f++) dmma884(acc[f][0], acc[f][1], a, Ys[(8 * (fj0 + f) + gq) * LDR + k + t]);
+    }
+#pragma unroll
+    for (int f = 0; f < 2; f++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) out[(8 * fi + gq) + 64 * (8 * (fj0 + f) + 2 * t + h)] = acc[f][h];
+  }
+}
+
+// Y(r, :) = (ACC ? Y(r, :) : 0) + A(r, :) B, A = As column-major (K columns), B = Bs[k * kRfHLD + j];
+// warps own 8-row tiles (all 32 columns), so the in-place A = Y case is race free.
+template <bool ACC>
+__device__ __forceinline__ void rf_rowmul(const double* As, double* Ys, int LDR, int R, int K, const double* Bs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t = lane & 3;
+  for (int rt = warp; rt < R / 8; rt += 8) {
+    const int r = 8 * rt + gq;
+    double acc[4][2];
+#pragma unroll
+    for (int f = 0; f < 4; f++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) acc[f][h] = ACC ? Ys[(8 * f + 2 * t + h) * LDR + r] : 0.0;
+    for (int k = 0; k < K; k += 4) {
+      const double a = As[(k + t) * LDR + r];
+#pragma unroll
+      for (int f = 0; f < 4; f++) dmma884(acc[f][0], acc[f][1], a, Bs[(k + t) * kRfHLD + 8 * f + gq]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 4; f++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) Ys[(8 * f + 2 * t + h) * LDR + r] = acc[f][h];
+  }
+}
+
+// cross-CTA sum of the partials (fixed order per element: lane-strided over CTAs, then a
+// warp tree), one element per warp, all warps of the grid
+__device__ __forceinline__ void rf_reduce(const double* part, int G, int cnt, double* H) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (blockDim.x >> 5);
+  for (int e = gw; e < cnt; e += nw) {
+    double v[kReorthMaxG / 32];
+#pragma unroll
+    for (int q = 0; q < kReorthMaxG / 32; q++) {   // all loads in flight, then a fixed-order sum
+      const int c = lane + 32 * q;
+      v[q] = (c < G) ? __ldcg(part + (size_t)c * kRfCnt + e) : 0.0;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kReorthMaxG / 32; q++) s += v[q];
+    s = warp_sum(s);
+    if (lane == 0) H[e] = s;
+  }
+}
+
+// columns [c0, c0 + nvalid) of Q, rows [r0, r0 + nr), into smem columns 0 .. ntot-1 (LDR);
+// rows nr..R-1 and columns nvalid..ntot-1 zero-filled.  cp.async: every copy in flight.
+__device__ __forceinline__ void rf_load_cols(double* dst, const double* Q, int64_t ldq, int64_t r0, int nr, int R,
+                                             int LDR, int64_t c0, int nvalid, int ntot) {
+  for (int j = 0; j < ntot; j++) {
+    const bool cv = j < nvalid;
+    const double* src = Q + SK_IDX(r0, c0 + (cv ? j : 0), ldq);
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      const bool ok = cv && r < nr;
+      cp_async8(dst + j * LDR + r, ok ? src + r : Q, ok ? 8 : 0);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+}
+
+__global__ void __launch_bounds__(256, 1) td_reorth_fused_kernel(ReorthArgs ra) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double rsm[];
+  const int LDR = ra.LDR, R = ra.R, G = gridDim.x;
+  double* Ys = rsm;                      // 32 x LDR
+  double* Qs = Ys + 32 * LDR;            // 64 x LDR
+  double* Bs = Qs + 64 * LDR;            // 64 x kRfHLD (-H, or (L^-1)^T)
+  double* Ls = Bs + 64 * kRfHLD;         // 32 x 33 Cholesky factor
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const int nr = (int)smax<int64_t>(0, smin<int64_t>(R, ra.n - r0));
+  double* mypart = ra.part + (size_t)blockIdx.x * kRfCnt;
+  double* Hg = ra.part + (size_t)G * kRfCnt;
+  // Qs columns 0..qcnt-1 hold this CTA's rows of the finished vectors [qcache, qcache + qcnt)
+  // (the previous block): the usual CGS window needs no reload
+  int64_t qcache = -1;
+  int qcnt = 0;
+  for (int b = 0; b < ra.nblk; b++) {
+    const int64_t k0 = ra.blk[3 * b], p0 = ra.blk[3 * b + 1];
+    const int nb = (int)ra.blk[3 * b + 2];
+    rf_load_cols(Ys, ra.Q, ra.ldq, r0, nr, R, LDR, k0, nb, 32);
+    __syncthreads();
+    // CGS2 against the previous vectors [p0, k0), chunks of <= 64
+    for (int pass = 0; pass < 2; pass++) {
+      for (int64_t q0 = p0; q0 < k0; q0 += 64) {
+        const int p = (int)smin<int64_t>(64, k0 - q0), p8 = (p + 7) & ~7;
+        if (!(q0 == qcache && p == qcnt)) {
+          rf_load_cols(Qs, ra.Q, ra.ldq, r0, nr, R, LDR, q0, p, p8);
+          qcache = -1;
+        }
+        __syncthreads();
+        rf_gram(Qs, Ys, LDR, R, p8 / 8, 0, mypart);
+        grid.sync();
+        rf_reduce(ra.part, G, 64 * 32, Hg);
+        grid.sync();
+#pragma unroll 8
+        for (int e = tid; e < 64 * 32; e += 256) {
+          const int i = e & 63, j = e >> 6;
+          if (i < p8) Bs[i * kRfHLD + j] = -__ldcg(Hg + e);
+        }
+        __syncthreads();
+        rf_rowmul<true>(Qs, Ys, LDR, R, p8, Bs);   // Y -= Qp H
+        __syncthreads();
+      }
+    }
+    // CholQR2 inside the block: G = Y^T Y = L L^T, Y <- Y L^-T
+    for (int pass = 0; pass < 2; pass++) {
+      rf_gram(Ys, Ys, LDR, R, 4, 1, mypart);
+      grid.sync();
+      rf_reduce(ra.part, G, 64 * 32, Hg);
+      grid.sync();
+      if (warp == 0) {
+        double a[32];
+#pragma unroll
+        for (int k = 0; k < 32; k++) a[k] = (lane < nb && k < nb) ? __ldcg(Hg + lane + 64 * k) : (lane == k ? 1.0 : 0.0);
+#pragma unroll
+        for (int j = 0; j < 32; j++) {   // right-looking Cholesky, lane i holds row i
+          const double d = sqrt(fmax(__shfl_sync(0xffffffffu, a[j], j), 1e-300));
+          const double lij = lane > j ? a[j] / d : (lane == j ? d : 0.0);
+          a[j] = lij;
+#pragma unroll
+          for (int k = j + 1; k < 32; k++) a[k] -= lij * __shfl_sync(0xffffffffu, lij, k);
+        }
+#pragma unroll
+        for (int k = 0; k < 32; k++) Ls[lane * 33 + k] = (k <= lane) ? a[k] : 0.0;
+        __syncwarp();
+        // lane j: column j of L^-1 by forward substitution (x_i = 0 for i < j)
+        double x[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+          double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+          for (int k = 0; k < i; k++) s -= Ls[i * 33 + k] * x[k];
+          x[i] = s / Ls[i * 33 + i];
+        }
+        // B(k, j) = (L^-1)(j, k):  lane j holds (L^-1)(., j) -> row j of B
+#pragma unroll
+        for (int k = 0; k < 32; k++) Bs[lane * kRfHLD + k] = x[k];
+      }
+      __syncthreads();
+      rf_rowmul<false>(Ys, Ys, LDR, R, 32, Bs);
+      __syncthreads();
+    }
+    for (int j = 0; j < 32; j++)   // write back, and keep the block as the next CGS window
+      for (int r = tid; r < R; r += 256) {
+        const double y = Ys[j * LDR + r];
+        if (j < nb && r < nr) ra.Q[SK_IDX(r0 + r, k0 + j, ra.ldq)] = y;
+        Qs[j * LDR + r] = y;
+      }
+    qcache = k0;
+    qcnt = nb;
+    __syncthreads();
+  }
+}
+
 static constexpr int kReorthNB = 32;
 static constexpr int64_t kGramRows = 128;
 
@@ -432,6 +643,8 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
   w.part = ar.take<double>((size_t)nchunks * p * kReorthNB + (size_t)p * kReorthNB);
   w.H = ar.take<double>((size_t)p * kReorthNB);
   w.Rinv = ar.take<double>((size_t)kReorthNB * kReorthNB);
+  w.rpart = ar.take<double>((size_t)(kReorthMaxG + 1) * kRfCnt);
+  w.rblk = ar.take<int64_t>((size_t)3 * ((ne + kReorthNB - 1) / kReorthNB + 1));
 }
 
 static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* Y, int64_t ldy, int nb, int64_t n,
@@ -581,8 +794,57 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
   }
   e = cudaGetLastError();
   if (e) return e;
-  // re-orthogonalisation in blocks of 32 (descending order)
-  for (int64_t k0 = vlo; k0 < vhi; k0 += kReorthNB) {
+  // re-orthogonalisation in blocks of 32 (descending order): one fused cooperative launch
+  // when the per-CTA row slices fit in shared memory, else the kernel-per-step sequence
+  bool fused = false;
+  {
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int G = (int)smin<int64_t>(smin<int64_t>(nsm, kReorthMaxG), smax<int64_t>(1, (n + 7) / 8));
+    const int R = (int)((((n + G - 1) / G) + 7) & ~int64_t(7));
+    const int LDR = R + (((4 - R) % 16) + 16) % 16;
+    const size_t smem = ((size_t)96 * LDR + 64 * kRfHLD + 32 * 33) * sizeof(double);
+    const char* fz = getenv("SKEWEIG_REORTH_FUSED");   // experiments: 0 = kernel-per-step path
+    fused = smem <= 227 * 1024 && !(fz && fz[0] == '0');
+    if (fused) {
+      static bool attr = false;
+      if (!attr) {
+        e = cudaFuncSetAttribute(td_reorth_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e) return e;
+        attr = true;
+      }
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, td_reorth_fused_kernel, 256, smem);
+      fused = occ * nsm >= G;
+    }
+    if (fused) {
+      std::vector<int64_t> blk;
+      for (int64_t k0 = vlo; k0 < vhi; k0 += kReorthNB) {
+        int64_t p0 = std::max<int64_t>(vlo, k0 - W);
+        const int64_t cs = std::max<int64_t>(vlo, clus_start[k0]);
+        if (cs < p0) p0 = cs;
+        blk.push_back(k0 - vlo);
+        blk.push_back(p0 - vlo);
+        blk.push_back(std::min<int64_t>(kReorthNB, vhi - k0));
+      }
+      const int nblk = (int)(blk.size() / 3);
+      if (nblk > 0) {
+        e = cudaMemcpyAsync(w.rblk, blk.data(), sizeof(int64_t) * blk.size(), cudaMemcpyHostToDevice, st);
+        if (e) return e;
+        ReorthArgs ra;
+        ra.Q = Q; ra.ldq = ldq; ra.n = n; ra.blk = w.rblk; ra.nblk = nblk; ra.part = w.rpart; ra.R = R; ra.LDR = LDR;
+        void* args[] = {&ra};
+        KScope ks(KC_TRID_REORTH, st);
+        e = cudaLaunchCooperativeKernel((void*)td_reorth_fused_kernel, dim3(G), dim3(256), args, smem, st);
+        if (e) return e;
+        // the host copy of blk must outlive the async copy
+        e = cudaStreamSynchronize(st);
+        if (e) return e;
+      }
+    }
+  }
+  if (!fused) for (int64_t k0 = vlo; k0 < vhi; k0 += kReorthNB) {
     int nb = (int)std::min<int64_t>(kReorthNB, vhi - k0);
     int64_t p0 = std::max<int64_t>(vlo, k0 - W);
     int64_t cs = std::max<int64_t>(vlo, clus_start[k0]);

@@ -280,3 +280,28 @@ def test_cholqr_panels_random(sk, n):
     assert st == 0
     lam, Zre, Zim = sk.skew_eig(_cuda(A))
     _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
+
+
+# ------------------------------------------------------------------ re-orthogonalisation paths
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_reorth_paths_clustered(sk, fused, monkeypatch):
+    """Clusters of 100 equal eigenvalues span several 32-vector blocks, so the CGS2 window
+    reaches back over > 64 vectors (chunked projections).  Both the fused cooperative
+    re-orthogonalisation (tridiag.cu td_reorth_fused_kernel) and the kernel-per-step path
+    must meet the tolerances (reading R9(4))."""
+    monkeypatch.setenv("SKEWEIG_REORTH_FUSED", fused)
+    sig = np.repeat(np.array([4.0, 3.0, 2.0, 1.0]), 100)
+    A = skewgen.planted_skew(sig, seed=11)
+    lam, Zre, Zim = sk.skew_eig(_cuda(A))
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), np.sort(sig)[::-1])
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_reorth_paths_random(sk, fused, monkeypatch):
+    monkeypatch.setenv("SKEWEIG_REORTH_FUSED", fused)
+    n = 1500
+    A = skewgen.random_skew(n, 4242)
+    lam_o, Zre_o, Zim_o, st = oracle.skew_eig(A)
+    assert st == 0
+    lam, Zre, Zim = sk.skew_eig(_cuda(A))
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)

@@ -44,6 +44,10 @@ int main() {
     run<64,64,32,32,32,2,false,true,true>("r2k", g, fl);
     run<64,32,16,32,16,4,false,true,true>("r2k", g, fl);
     run<64,64,16,16,32,4,false,true,true>("r2k", g, fl);
+    run<128,64,16,32,32,3,false,true,true>("r2k", g, fl);
+    run<128,64,16,64,32,3,false,true,true>("r2k", g, fl);
+    run<128,128,16,64,32,3,false,true,true>("r2k", g, fl);
+    run<128,128,16,32,64,3,false,true,true>("r2k", g, fl);
   }
   {  // Z = U^T X : M = 256, N = n, K = n
     GemmArgs g{}; g.M = K2; g.N = n; g.K = n; g.A = U; g.lda = n; g.B = A; g.ldb = n; g.C = Z; g.ldc = K2;
@@ -54,6 +58,10 @@ int main() {
     run<64,64,32,32,32,2,true,false,false>("bt1 z", g, fl);
     run<64,32,16,32,16,4,true,false,false>("bt1 z", g, fl);
     run<64,64,16,16,32,4,true,false,false>("bt1 z", g, fl);
+    run<128,64,16,32,32,3,true,false,false>("bt1 z", g, fl);
+    run<128,64,16,64,32,3,true,false,false>("bt1 z", g, fl);
+    run<128,128,16,64,32,3,true,false,false>("bt1 z", g, fl);
+    run<128,128,16,32,64,3,true,false,false>("bt1 z", g, fl);
   }
   {  // X -= V Z : M = n, N = n, K = 256
     GemmArgs g{}; g.M = n; g.N = n; g.K = K2; g.A = U; g.lda = n; g.B = Z; g.ldb = K2; g.C = A; g.ldc = n;
@@ -64,6 +72,10 @@ int main() {
     run<64,64,32,32,32,2,false,false,false>("bt1 update", g, fl);
     run<64,32,16,32,16,4,false,false,false>("bt1 update", g, fl);
     run<64,64,16,16,32,4,false,false,false>("bt1 update", g, fl);
+    run<128,64,16,32,32,3,false,false,false>("bt1 update", g, fl);
+    run<128,64,16,64,32,3,false,false,false>("bt1 update", g, fl);
+    run<128,128,16,64,32,3,false,false,false>("bt1 update", g, fl);
+    run<128,128,16,32,64,3,false,false,false>("bt1 update", g, fl);
   }
   return 0;
 }
