@@ -96,6 +96,23 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Grid-wide barrier for a cooperative (all CTAs co-resident) launch: one arrival per CTA on a
+// monotonically increasing counter that is zeroed before the launch; `epoch` is the caller's
+// running target (+gridDim.x per barrier).  gpu-scope fences around the arrival / the poll.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& epoch) {
+  __syncthreads();
+  epoch += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < epoch);
+    __threadfence();
+  }
+  __syncthreads();
+}
 __device__ __forceinline__ void fence_acqrel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // generic-proxy accesses (all state spaces) ordered before later async-proxy (bulk/TMA) ones
 __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }

@@ -59,11 +59,11 @@ struct PanelArgs {
   double* gram;                // [G][kb*kb] partial Gram, then [kb*kb] final
   int64_t R;                   // rows per CTA
   int smem_rows;               // R if the CTA rows live in shared memory, else 0
+  unsigned* gbar;              // grid barrier counter (zeroed before each launch; common.cuh grid_barrier)
 };
 
 template <bool SMEM>
-__device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm) {
-  cg::grid_group grid = cg::this_grid();
+__device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm, unsigned& bar_epoch) {
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kb = a.kb;
   const int64_t rb = (int64_t)cta * a.R;
@@ -112,7 +112,7 @@ __device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm) {
   };
   partials(0);
   __threadfence();
-  grid.sync();
+  grid_barrier(a.gbar, bar_epoch);
   const int kmax = (int)smin<int64_t>(kb, a.m);
   for (int k = 0; k < kmax; k++) {
     const int buf = k & 1;
@@ -177,7 +177,7 @@ __device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm) {
     if (k + 1 < kmax) {
       partials(k + 1);
       __threadfence();
-      grid.sync();
+      grid_barrier(a.gbar, bar_epoch);
     }
   }
   // columns kmax..kb-1 (only when m < kb): identity reflectors
@@ -230,7 +230,7 @@ __device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm) {
         if (r0 + i < kb && c0 + j < kb) a.gram[(size_t)cta * kb * kb + (r0 + i) + (c0 + j) * kb] = g4[i][j];
   }
   __threadfence();
-  grid.sync();
+  grid_barrier(a.gbar, bar_epoch);
   double* gfin = a.gram + (size_t)G * kb * kb;
   for (int e = blockIdx.x * blockDim.x + tid; e < kb * kb; e += G * blockDim.x) {
     double s = 0.0;
@@ -239,7 +239,7 @@ __device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm) {
     gfin[e] = s;
   }
   __threadfence();
-  grid.sync();
+  grid_barrier(a.gbar, bar_epoch);
   // T (forward, columnwise dlarft): T[c][c] = tau_c, T[0:c, c] = -tau_c T[0:c,0:c] G[0:c, c]
   if (cta == 0) {
     const int LDG = kb + 1;                 // odd: conflict-free row/column sweeps
@@ -270,7 +270,8 @@ __device__ __noinline__ void panel_householder(const PanelArgs& a, double* sm) {
 template <bool SMEM>
 __global__ void __launch_bounds__(256) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double sm[];
-  panel_householder<SMEM>(a, sm);
+  unsigned bar_epoch = 0;
+  panel_householder<SMEM>(a, sm, bar_epoch);
 }
 
 // ------------------------------------------------------------------------------------
@@ -296,7 +297,7 @@ struct CqrArgs {
 
 template <int KB>
 __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned bar_epoch = 0;
   extern __shared__ __align__(16) double sm[];
   const PanelArgs& a = ca.p;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
       for (int j = 0; j < 4; j++) a.gram[(size_t)cta * KB * KB + (p + 16 * i) + (q + 16 * j) * KB] = g4[i][j];
     TS();
     __threadfence();
-    grid.sync();
+    grid_barrier(a.gbar, bar_epoch);
     TS();
     {
       const int per = (KB * KB + G - 1) / G;   // entries of this CTA: [cta*per, cta*per + per)
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
       }
     }
     __threadfence();
-    grid.sync();
+    grid_barrier(a.gbar, bar_epoch);
     TS();
   };
   // CTA 0: kb x kb rank-1 trailing update Ms[r][c] -= x_r y_c over rows/cols > k (c >= r
@@ -490,14 +491,14 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
     }
     TS();
     __threadfence();
-    grid.sync();
+    grid_barrier(a.gbar, bar_epoch);
     ok = __ldcg(&gflag[0]) == 0.0;
     if (ok) trsm_rows(gR1);
     TS();
   }
   if (!ok) {   // ill-conditioned or rank-deficient panel: Householder, same launch
     __syncthreads();
-    panel_householder<true>(a, sm);
+    panel_householder<true>(a, sm, bar_epoch);
     return;
   }
   // ---- Householder reconstruction: CTA 0 holds rows 0..kb-1 (R >= kb)
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
   }
   TS();
   __threadfence();
-  grid.sync();
+  grid_barrier(a.gbar, bar_epoch);
   TS();
   // V: rows >= kb: y = q U^-1 (row solve with U upper, right-looking); rows < kb: L1
   for (int e = tid; e < KB * KB; e += blockDim.x) Ms2[(e / KB) * LDK + e % KB] = __ldcg(&gU[e]);
@@ -883,6 +884,7 @@ void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w, int P) {
   w.zpart = ar.take<double>(((n + kWRows - 1) / kWRows + 2) * b * b);
   w.Mb = ar.take<double>(b * b);
   w.cqr = ar.take<double>(3 * (size_t)b * b + b + 2);
+  w.gbar = ar.take<unsigned>(64);
   w.Ycol = ar.take<double>((size_t)std::max(P, kSymmMaxSplit) * ldn * b);
 }
 
@@ -903,6 +905,7 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   a.A = A + SK_IDX(r0, c0, lda); a.lda = lda; a.m = m; a.kb = b;
   a.V = Vj; a.ldv = ldv; a.tau = w.tau + j * b; a.T = w.T + j * (int64_t)b * b; a.ldt = b;
   a.part = w.part; a.rowk = w.rowk; a.gram = w.gram;
+  a.gbar = w.gbar;
   int G = panel_grid(m, nsm);
   a.R = (m + G - 1) / G;
   size_t extra = (size_t)(8 * (b + 1) + (b + 1) + b + 4) * sizeof(double);
@@ -912,7 +915,8 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   if (!use_smem) extra = std::max(extra, tbuild);
   a.smem_rows = use_smem ? (int)a.R : 0;
   void* args[] = {&a};
-  cudaError_t e;
+  cudaError_t e = cudaMemsetAsync(w.gbar, 0, sizeof(unsigned), st);
+  if (e) return e;
   KScope ks(KC_PANEL, st);
   // CholeskyQR2 + reconstruction when CTA 0 holds the top b rows and the rows fit in smem
   // (its own grid: floor(m/b) CTAs at most, so that every CTA -- CTA 0 in particular --

@@ -131,6 +131,7 @@ struct F2BWork {
   double* zpart = nullptr;   // V^T X partials
   double* Mb = nullptr;      // b x b
   double* cqr = nullptr;     // CholeskyQR panel scratch (3 b^2 + b + 2)
+  unsigned* gbar = nullptr;  // panel grid barrier counter
   double* Ycol = nullptr;    // distributed skew-SYMM column-part pieces (P x n x b)
 };
 
@@ -167,6 +168,7 @@ struct TridWork {
   double* Rinv = nullptr;
   double* rpart = nullptr;     // fused reorthogonalisation: per-CTA Gram partials + reduced H
   int64_t* rblk = nullptr;     // fused reorthogonalisation: per 32-vector block (k0, p0, nb)
+  unsigned* gbar = nullptr;    // fused reorthogonalisation: grid barrier counter
   int64_t batch = 0;
 };
 

@@ -425,6 +425,8 @@ struct ReorthArgs {
   const int64_t* blk; int nblk;   // per block: k0, p0, nb (columns relative to Q)
   double* part;                    // G x kRfCnt partials, then kRfCnt reduced
   int R, LDR;                      // rows per CTA (multiple of 8), smem column stride
+  long long* dbg = nullptr;        // optional phase timing (SKEWEIG_REORTH_DBG), CTA 0
+  unsigned* gbar = nullptr;        // grid barrier counter (zeroed before the launch)
 };
 
 // partial Gram: out(i, j) = sum_r X(r, i) Y(r, j), i < 8*FI (X columns), j < 32; X, Y column-major
@@ -524,7 +526,7 @@ __device__ __forceinline__ void rf_load_cols(double* dst, const double* Q, int64
 }
 
 __global__ void __launch_bounds__(256, 1) td_reorth_fused_kernel(ReorthArgs ra) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned bar_epoch = 0;
   extern __shared__ __align__(16) double rsm[];
   const int LDR = ra.LDR, R = ra.R, G = gridDim.x;
   double* Ys = rsm;                      // 32 x LDR
@@ -540,6 +542,9 @@ __global__ void __launch_bounds__(256, 1) td_reorth_fused_kernel(ReorthArgs ra) 
   // (the previous block): the usual CGS window needs no reload
   int64_t qcache = -1;
   int qcnt = 0;
+  const bool prof = ra.dbg != nullptr && blockIdx.x == 0 && tid == 0;
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp = prof ? clock64() : 0;
+#define RF_TS(k) do { if (prof) { long long _t = clock64(); ph[k] += _t - tp; tp = _t; } } while (0)
   for (int b = 0; b < ra.nblk; b++) {
     const int64_t k0 = ra.blk[3 * b], p0 = ra.blk[3 * b + 1];
     const int nb = (int)ra.blk[3 * b + 2];
@@ -554,56 +559,73 @@ __global__ void __launch_bounds__(256, 1) td_reorth_fused_kernel(ReorthArgs ra) 
           qcache = -1;
         }
         __syncthreads();
+        RF_TS(0);
         rf_gram(Qs, Ys, LDR, R, p8 / 8, 0, mypart);
-        grid.sync();
+        RF_TS(1);
+        grid_barrier(ra.gbar, bar_epoch);
+        RF_TS(2);
         rf_reduce(ra.part, G, 64 * 32, Hg);
-        grid.sync();
+        RF_TS(3);
+        grid_barrier(ra.gbar, bar_epoch);
+        RF_TS(2);
 #pragma unroll 8
         for (int e = tid; e < 64 * 32; e += 256) {
           const int i = e & 63, j = e >> 6;
           if (i < p8) Bs[i * kRfHLD + j] = -__ldcg(Hg + e);
         }
         __syncthreads();
+        RF_TS(0);
         rf_rowmul<true>(Qs, Ys, LDR, R, p8, Bs);   // Y -= Qp H
+        RF_TS(4);
         __syncthreads();
       }
     }
     // CholQR2 inside the block: G = Y^T Y = L L^T, Y <- Y L^-T
     for (int pass = 0; pass < 2; pass++) {
+      RF_TS(0);
       rf_gram(Ys, Ys, LDR, R, 4, 1, mypart);
-      grid.sync();
+      RF_TS(1);
+      grid_barrier(ra.gbar, bar_epoch);
+      RF_TS(2);
       rf_reduce(ra.part, G, 64 * 32, Hg);
-      grid.sync();
+      RF_TS(3);
+      grid_barrier(ra.gbar, bar_epoch);
+      RF_TS(2);
       if (warp == 0) {
         double a[32];
 #pragma unroll
         for (int k = 0; k < 32; k++) a[k] = (lane < nb && k < nb) ? __ldcg(Hg + lane + 64 * k) : (lane == k ? 1.0 : 0.0);
+        double rdiag = 1.0;   // lane j: 1 / L_jj
 #pragma unroll
-        for (int j = 0; j < 32; j++) {   // right-looking Cholesky, lane i holds row i
-          const double d = sqrt(fmax(__shfl_sync(0xffffffffu, a[j], j), 1e-300));
-          const double lij = lane > j ? a[j] / d : (lane == j ? d : 0.0);
+        for (int j = 0; j < 32; j++) {   // right-looking Cholesky, lane i holds row i (no divisions)
+          const double r = rsqrt(fmax(__shfl_sync(0xffffffffu, a[j], j), 1e-300));
+          const double lij = lane >= j ? a[j] * r : 0.0;   // lane j: d * rsqrt(d) = sqrt(d)
+          if (lane == j) rdiag = r;
           a[j] = lij;
 #pragma unroll
           for (int k = j + 1; k < 32; k++) a[k] -= lij * __shfl_sync(0xffffffffu, lij, k);
         }
 #pragma unroll
-        for (int k = 0; k < 32; k++) Ls[lane * 33 + k] = (k <= lane) ? a[k] : 0.0;
+        for (int k = 0; k < 32; k++) Ls[lane * 33 + k] = (k < lane) ? a[k] : (k == lane ? rdiag : 0.0);
         __syncwarp();
-        // lane j: column j of L^-1 by forward substitution (x_i = 0 for i < j)
+        // lane j: column j of L^-1 by forward substitution (x_i = 0 for i < j); Ls holds
+        // 1 / L_ii on its diagonal
         double x[32];
 #pragma unroll
         for (int i = 0; i < 32; i++) {
           double s = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
           for (int k = 0; k < i; k++) s -= Ls[i * 33 + k] * x[k];
-          x[i] = s / Ls[i * 33 + i];
+          x[i] = s * Ls[i * 33 + i];
         }
         // B(k, j) = (L^-1)(j, k):  lane j holds (L^-1)(., j) -> row j of B
 #pragma unroll
         for (int k = 0; k < 32; k++) Bs[lane * kRfHLD + k] = x[k];
       }
       __syncthreads();
+      RF_TS(5);
       rf_rowmul<false>(Ys, Ys, LDR, R, 32, Bs);
+      RF_TS(4);
       __syncthreads();
     }
     for (int j = 0; j < 32; j++)   // write back, and keep the block as the next CGS window
@@ -615,7 +637,10 @@ __global__ void __launch_bounds__(256, 1) td_reorth_fused_kernel(ReorthArgs ra) 
     qcache = k0;
     qcnt = nb;
     __syncthreads();
+    RF_TS(6);
   }
+  if (prof) for (int k = 0; k < 8; k++) ra.dbg[k] = ph[k];
+#undef RF_TS
 }
 
 static constexpr int kReorthNB = 32;
@@ -645,6 +670,7 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
   w.Rinv = ar.take<double>((size_t)kReorthNB * kReorthNB);
   w.rpart = ar.take<double>((size_t)(kReorthMaxG + 1) * kRfCnt);
   w.rblk = ar.take<int64_t>((size_t)3 * ((ne + kReorthNB - 1) / kReorthNB + 1));
+  w.gbar = ar.take<unsigned>(64);
 }
 
 static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* Y, int64_t ldy, int nb, int64_t n,
@@ -834,10 +860,23 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
         if (e) return e;
         ReorthArgs ra;
         ra.Q = Q; ra.ldq = ldq; ra.n = n; ra.blk = w.rblk; ra.nblk = nblk; ra.part = w.rpart; ra.R = R; ra.LDR = LDR;
+        ra.gbar = w.gbar;
+        e = cudaMemsetAsync(w.gbar, 0, sizeof(unsigned), st);
+        if (e) return e;
+        static long long* dbgp = nullptr;
+        if (getenv("SKEWEIG_REORTH_DBG") && !dbgp) cudaMalloc(&dbgp, 8 * sizeof(long long));   // debug only
+        ra.dbg = getenv("SKEWEIG_REORTH_DBG") ? dbgp : nullptr;
         void* args[] = {&ra};
         KScope ks(KC_TRID_REORTH, st);
         e = cudaLaunchCooperativeKernel((void*)td_reorth_fused_kernel, dim3(G), dim3(256), args, smem, st);
         if (e) return e;
+        if (ra.dbg) {
+          long long h[8];
+          cudaMemcpyAsync(h, ra.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          fprintf(stderr, "[reorth dbg] G=%d R=%d nblk=%d cycles: misc %lld gram %lld sync %lld reduce %lld rowmul %lld "
+                  "chol %lld writeback %lld\n", G, R, nblk, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+        }
         // the host copy of blk must outlive the async copy
         e = cudaStreamSynchronize(st);
         if (e) return e;
