@@ -195,6 +195,12 @@ int skew_ctx_create_dist(skew_ctx* out, int device, void* cuda_stream, int nrank
 int skew_ctx_destroy(skew_ctx ctx) {
   if (!ctx) return -1;
   if (ctx->c.nccl) ncclCommDestroy((ncclComm_t)ctx->c.nccl);
+  if (ctx->c.aux) {
+    cudaStreamSynchronize(ctx->c.aux);
+    cudaStreamDestroy(ctx->c.aux);
+    cudaEventDestroy(ctx->c.ev_fork);
+    cudaEventDestroy(ctx->c.ev_join);
+  }
   for (int s = 0; s < ST_COUNT; s++) { cudaEventDestroy(ctx->ev_start[s]); cudaEventDestroy(ctx->ev_stop[s]); }
   delete ctx;
   return SKEW_OK;
@@ -273,6 +279,12 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   cudaStream_t st = c.stream;
   const int64_t n = p.n;
   const bool vec = (Zre != nullptr);
+  if (vec && p.f2b.npanel > 0) CK(bt1_upload_meta(p.f2b, p.b1, st), "bt1 meta");
+  if (vec && !c.aux) {
+    CK(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking), "aux stream");
+    CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
+    CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
+  }
   // ---- full -> band
   tstart(ctx, ST_F2B);
   Dist d;
@@ -294,6 +306,13 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   }
   CK(b2t_run(p.b2t, p.bw, p.alpha, c.num_sms, st), "b2t");
   tstop(ctx, ST_B2T);
+  if (vec) {   // BT2 / BT1 preparation on the auxiliary stream, concurrent with the tridiagonal solve
+    CK(cudaEventRecord(c.ev_fork, st), "fork");
+    CK(cudaStreamWaitEvent(c.aux, c.ev_fork, 0), "fork wait");
+    CK(bt2_prep(p.b2t, p.bw, c.aux), "bt2 prep");
+    if (p.f2b.npanel > 0) CK(bt1_prep(p.f2b, p.vstore, p.fw.T, p.b1, c.aux), "bt1 prep");
+    CK(cudaEventRecord(c.ev_join, c.aux), "join");
+  }
   // ---- tridiagonal eigenproblem
   tstart(ctx, ST_TRID);
   int64_t nfail = 0;
@@ -308,11 +327,12 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   }
   tstop(ctx, ST_TRID);
   if (vec) {
+    CK(cudaStreamWaitEvent(st, c.ev_join, 0), "join wait");
     tstart(ctx, ST_BT2);
-    CK(bt2_run(p.b2t, p.bw, p.X, p.ldn, 2 * nloc, st), "bt2");
+    CK(bt2_apply(p.b2t, p.bw, p.X, p.ldn, 2 * nloc, st), "bt2");
     tstop(ctx, ST_BT2);
     tstart(ctx, ST_BT1);
-    if (p.f2b.npanel > 0) CK(bt1_run(p.f2b, p.vstore, p.fw.tau, p.fw.T, p.X, p.ldn, 2 * nloc, p.b1, st), "bt1");
+    if (p.f2b.npanel > 0) CK(bt1_apply(p.f2b, p.vstore, p.fw.tau, p.fw.T, p.X, p.ldn, 2 * nloc, p.b1, st), "bt1");
     tstop(ctx, ST_BT1);
   }
   // ---- output

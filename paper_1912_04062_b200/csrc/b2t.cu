@@ -423,6 +423,121 @@ struct BT2Cfg {
   static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && (NB == 64 || NB == 32), "ring");
 };
 
+// ring slot of (column, slot) with the bank swizzle of the window ring
+template <int NB, int K2, int RW, int RING, int BB>
+__device__ __forceinline__ int bt2_xo(int col, int slot) {
+  return col * BT2Cfg<NB, K2, RW, RING, BB>::LDX + (slot ^ (((col >> 2) & 1) << 2));
+}
+
+// Z = U^T Xw (K2 x NB): warp (h, column quarter); U[rho][c] = 0 for rho <= c skipped at
+// compile time (H = h); even / odd k-step accumulator sets; next fragments loaded first.
+template <int NB, int K2, int RW, int RING, int H>
+__device__ __forceinline__ void bt2_gemm1(const double* Xs, const double* Us, double* Zs, int off, int warp, int gq,
+                                          int tq) {
+  using C = BT2Cfg<NB, K2, RW, RING, 64>;
+  constexpr int FN = NB / 32;          // column fragments per warp
+  constexpr int NIT = RW / 8;
+  const int n0 = (warp >> 1) * (NB / 4);
+  double acc[2][2][FN][2];
+#pragma unroll
+  for (int p = 0; p < 2; p++)
+#pragma unroll
+    for (int i = 0; i < 2; i++)
+#pragma unroll
+      for (int j = 0; j < FN; j++) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
+  double fa[2][2][2], fb[2][FN][2];
+  auto ld1 = [&](int it, int sb) {
+    const int kk = it * 8;
+    int slot = off + kk;
+    if (slot >= RING) slot -= RING;
+#pragma unroll
+    for (int j = 0; j < FN; j++) {
+      fb[sb][j][0] = Xs[bt2_xo<NB, K2, RW, RING, 64>(n0 + 8 * j + gq, slot + tq)];
+      fb[sb][j][1] = Xs[bt2_xo<NB, K2, RW, RING, 64>(n0 + 8 * j + gq, slot + 4 + tq)];
+    }
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      if (it * 8 + 7 < 8 * (H + 2 * i)) continue;   // fragment entirely zero: not needed
+      const int c = 8 * (H + 2 * i) + gq;
+      fa[sb][i][0] = Us[c * C::LDW + kk + tq];
+      fa[sb][i][1] = Us[c * C::LDW + kk + 4 + tq];
+    }
+  };
+  ld1(0, 0);
+#pragma unroll
+  for (int it = 0; it < NIT; it++) {
+    const int sb = it & 1;
+    if (it + 1 < NIT) ld1(it + 1, sb ^ 1);
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      if (it * 8 + 7 < 8 * (H + 2 * i)) continue;   // U[rho][c] = 0 for rho <= c
+#pragma unroll
+      for (int j = 0; j < FN; j++) {
+        dmma884(acc[0][i][j][0], acc[0][i][j][1], fa[sb][i][0], fb[sb][j][0]);
+        dmma884(acc[1][i][j][0], acc[1][i][j][1], fa[sb][i][1], fb[sb][j][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < FN; j++) {
+      const int c = 8 * (H + 2 * i) + gq, nn = n0 + 8 * j + 2 * tq;
+      Zs[nn * C::LDZ + c] = acc[0][i][j][0] + acc[1][i][j][0];
+      Zs[(nn + 1) * C::LDZ + c] = acc[0][i][j][1] + acc[1][i][j][1];
+    }
+}
+
+// Xw -= V Z (RW x NB, K = K2): warp (wm = WM, column half); V[rho][c] != 0 iff
+// 1 <= rho - c <= BB, zero fragments skipped at compile time.
+template <int NB, int K2, int RW, int RING, int BB, int WM>
+__device__ __forceinline__ void bt2_gemm2(double* Xs, const double* Vs, const double* Zs, int off, int warp, int gq,
+                                          int tq) {
+  using C = BT2Cfg<NB, K2, RW, RING, BB>;
+  constexpr int FM = RW / 32, FN = NB / 16;
+  constexpr int NIT = K2 / 4;
+  const int n0 = (warp >> 2) * (NB / 2);
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; i++)
+#pragma unroll
+    for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double fa[2][FM], fb[2][FN];
+  auto live = [](int i, int kk) { const int m0 = 8 * (WM + 4 * i); return !(m0 + 7 - kk < 1 || m0 - (kk + 3) > BB); };
+  auto ld2 = [&](int it, int sb) {
+    const int kk = it * 4;
+#pragma unroll
+    for (int j = 0; j < FN; j++) fb[sb][j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
+#pragma unroll
+    for (int i = 0; i < FM; i++)
+      if (live(i, kk)) fa[sb][i] = Vs[(kk + tq) * C::LDW + 8 * (WM + 4 * i) + gq];
+  };
+  ld2(0, 0);
+#pragma unroll
+  for (int it = 0; it < NIT; it++) {
+    const int sb = it & 1, kk = it * 4;
+    if (it + 1 < NIT) ld2(it + 1, sb ^ 1);
+#pragma unroll
+    for (int i = 0; i < FM; i++) {
+      if (!live(i, kk)) continue;
+#pragma unroll
+      for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], fa[sb][i], fb[sb][j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < FM; i++) {
+    const int m0 = 8 * (WM + 4 * i);
+    int slot = off + m0;
+    if (slot >= RING) slot -= RING;
+#pragma unroll
+    for (int j = 0; j < FN; j++) {
+      const int nn = n0 + 8 * j + 2 * tq;
+      Xs[bt2_xo<NB, K2, RW, RING, BB>(nn, slot + gq)] -= acc[i][j][0];
+      Xs[bt2_xo<NB, K2, RW, RING, BB>(nn + 1, slot + gq)] -= acc[i][j][1];
+    }
+  }
+}
+
 // Warp-specialised: 8 consumer warps run only the two DMMA tiles per step; 4 producer warps
 // move the data one step ahead -- it waits until the consumers
 // released step q-1 (mbarrier "empty"), writes that step's leaving rows back to X, then
@@ -572,106 +687,19 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
     const double* Us = G0 + (q & 1) * C::GS;
     const double* Vs = Us + K2 * C::LDW;
       // ---- Z = U^T Xw : warps 2 (M: c fragments {h, h+2}, interleaved to balance U's zero
-      //      upper triangle) x 4 (N: NB/4 columns); even / odd k-step accumulator sets; next
-      //      fragments loaded before the current DMMAs.
-      {
-        constexpr int FN = NB / 32;          // 2 column fragments per warp
-        constexpr int NIT = RW / 8;
-        const int h = warp & 1, n0 = (warp >> 1) * (NB / 4);
-        double acc[2][2][FN][2];
-#pragma unroll
-        for (int p = 0; p < 2; p++)
-#pragma unroll
-          for (int i = 0; i < 2; i++)
-#pragma unroll
-            for (int j = 0; j < FN; j++) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
-        double fa[2][2][2], fb[2][FN][2];
-        auto ld1 = [&](int it, int sb) {
-          const int kk = it * 8;
-          int slot = off + kk;
-          if (slot >= RING) slot -= RING;
-#pragma unroll
-          for (int j = 0; j < FN; j++) {
-            fb[sb][j][0] = Xs[xo(n0 + 8 * j + gq, slot + tq)];
-            fb[sb][j][1] = Xs[xo(n0 + 8 * j + gq, slot + 4 + tq)];
-          }
-#pragma unroll
-          for (int i = 0; i < 2; i++) {
-            const int c = 8 * (h + 2 * i) + gq;
-            fa[sb][i][0] = Us[c * C::LDW + kk + tq];
-            fa[sb][i][1] = Us[c * C::LDW + kk + 4 + tq];
-          }
-        };
-        ld1(0, 0);
-#pragma unroll
-        for (int it = 0; it < NIT; it++) {
-          const int sb = it & 1;
-          if (it + 1 < NIT) ld1(it + 1, sb ^ 1);
-#pragma unroll
-          for (int i = 0; i < 2; i++) {
-            if (it * 8 + 7 < 8 * (h + 2 * i)) continue;   // U[rho][c] = 0 for rho <= c
-#pragma unroll
-            for (int j = 0; j < FN; j++) {
-              dmma884(acc[0][i][j][0], acc[0][i][j][1], fa[sb][i][0], fb[sb][j][0]);
-              dmma884(acc[1][i][j][0], acc[1][i][j][1], fa[sb][i][1], fb[sb][j][1]);
-            }
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 2; i++)
-#pragma unroll
-          for (int j = 0; j < FN; j++) {
-            const int c = 8 * (h + 2 * i) + gq, nn = n0 + 8 * j + 2 * tq;
-            Zs[nn * C::LDZ + c] = acc[0][i][j][0] + acc[1][i][j][0];
-            Zs[(nn + 1) * C::LDZ + c] = acc[0][i][j][1] + acc[1][i][j][1];
-          }
-      }
+      //      upper triangle) x 4 (N: NB/4 columns).  The zero-fragment pattern depends on h
+      //      only: compile-time per h, so skipped fragments issue nothing.
+      if (warp & 1) bt2_gemm1<NB, K2, RW, RING, 1>(Xs, Us, Zs, off, warp, gq, tq);
+      else bt2_gemm1<NB, K2, RW, RING, 0>(Xs, Us, Zs, off, warp, gq, tq);
       named_bar(1 + (warp >> 2), 128);   // two independent 4-warp groups (columns 0-31 / 32-63)
       BT2_TS(2);
-      // ---- Xw -= V Z : M = RW (rho), N = NB, K = K2 (c); warps 4 (M, interleaved row
-      //      fragments: balanced staircase work) x 2 (N); zero staircase fragments skipped.
-      {
-        constexpr int FM = RW / 32, FN = NB / 16;
-        constexpr int NIT = K2 / 4;
-        const int wm = warp & 3, n0 = (warp >> 2) * (NB / 2);
-        double acc[FM][FN][2];
-#pragma unroll
-        for (int i = 0; i < FM; i++)
-#pragma unroll
-          for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-        double fa[2][FM], fb[2][FN];
-        auto ld2 = [&](int it, int sb) {
-          const int kk = it * 4;
-#pragma unroll
-          for (int j = 0; j < FN; j++) fb[sb][j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
-#pragma unroll
-          for (int i = 0; i < FM; i++) fa[sb][i] = Vs[(kk + tq) * C::LDW + 8 * (wm + 4 * i) + gq];
-        };
-        ld2(0, 0);
-#pragma unroll
-        for (int it = 0; it < NIT; it++) {
-          const int sb = it & 1, kk = it * 4;
-          if (it + 1 < NIT) ld2(it + 1, sb ^ 1);
-#pragma unroll
-          for (int i = 0; i < FM; i++) {
-            const int m0 = 8 * (wm + 4 * i);
-            if (m0 + 7 - kk < 1 || m0 - (kk + 3) > BB) continue;   // V[rho][c] != 0 iff 1 <= rho - c <= BB
-#pragma unroll
-            for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], fa[sb][i], fb[sb][j]);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < FM; i++) {
-          const int m0 = 8 * (wm + 4 * i);
-          int slot = off + m0;
-          if (slot >= RING) slot -= RING;
-#pragma unroll
-          for (int j = 0; j < FN; j++) {
-            int nn = n0 + 8 * j + 2 * tq;
-            Xs[xo(nn, slot + gq)] -= acc[i][j][0];
-            Xs[xo(nn + 1, slot + gq)] -= acc[i][j][1];
-          }
-        }
+      // ---- Xw -= V Z : warps 4 (M, interleaved row fragments: balanced staircase work) x 2
+      //      (N); the staircase pattern depends on wm only: compile-time per wm.
+      switch (warp & 3) {
+        case 0: bt2_gemm2<NB, K2, RW, RING, BB, 0>(Xs, Vs, Zs, off, warp, gq, tq); break;
+        case 1: bt2_gemm2<NB, K2, RW, RING, BB, 1>(Xs, Vs, Zs, off, warp, gq, tq); break;
+        case 2: bt2_gemm2<NB, K2, RW, RING, BB, 2>(Xs, Vs, Zs, off, warp, gq, tq); break;
+        default: bt2_gemm2<NB, K2, RW, RING, BB, 3>(Xs, Vs, Zs, off, warp, gq, tq); break;
       }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[q & 1]);
@@ -785,16 +813,30 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
 
 static constexpr double kNB32Cost = 0.55;   // per-strip time of a 32-wide strip / a 64-wide one
 
+static constexpr int kBT2K2 = 32, kBT2RW = 96, kBT2Ring = 192, kBT2BB = 64;
+
+// [U | V] blocks of every group (depends only on the chase output: the solve driver runs it
+// on an auxiliary stream, concurrently with the tridiagonal solve)
+cudaError_t bt2_prep(const B2TLayout& L, B2TWork& w, cudaStream_t st) {
+  if (L.n <= 2 || L.ngroups == 0) return cudaSuccess;
+  if (L.k2 != kBT2K2 || L.b != kBT2BB) return cudaErrorInvalidValue;
+  KScope ks(KC_BT2_T, st);
+  bt2_prep_kernel<kBT2K2, kBT2RW><<<(unsigned)std::min<int64_t>(L.ngroups, 8 * 148), 128, 0, st>>>(
+      w.qv, w.qtau, L.ngroups, kBT2BB, w.qT);
+  return cudaGetLastError();
+}
+
 cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st) {
+  cudaError_t e = bt2_prep(L, w, st);
+  if (e) return e;
+  return bt2_apply(L, w, X, ldx, ncols, st);
+}
+
+cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st) {
   if (L.n <= 2 || L.ngroups == 0 || ncols == 0) return cudaSuccess;
   cudaError_t e;
-  constexpr int K2 = 32, RW = 96, RING = 192, BB = 64;
+  constexpr int K2 = kBT2K2, RW = kBT2RW, RING = kBT2Ring, BB = kBT2BB;
   if (L.k2 != K2 || L.b != BB) return cudaErrorInvalidValue;
-  {
-    KScope ks(KC_BT2_T, st);
-    bt2_prep_kernel<K2, RW><<<(unsigned)std::min<int64_t>(L.ngroups, 8 * 148), 128, 0, st>>>(w.qv, w.qtau, L.ngroups,
-                                                                                              BB, w.qT);
-  }
   long long* dbgp = nullptr;
   if (getenv("SKEWEIG_BT2_DBG")) cudaMalloc(&dbgp, 6 * sizeof(long long));   // debug instrumentation only
   // Column strips: 64 wide (best DMMA / smem ratio) and 32 wide (~0.55x the time of a

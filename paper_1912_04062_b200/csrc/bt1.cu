@@ -104,29 +104,49 @@ void bt1_reserve(Arena& ar, const F2BLayout& L, int64_t ncols, BT1Work& w) {
   w.gmeta = ar.take<int64_t>((size_t)3 * ng);
 }
 
+// per-group metadata (V-store offset, ld, rows) -> device; host-synchronous (call it before
+// the stream has work queued, e.g. at the start of the solve)
+cudaError_t bt1_upload_meta(const F2BLayout& L, BT1Work& w, cudaStream_t st) {
+  if (L.ngroup == 0) return cudaSuccess;
+  std::vector<int64_t> meta(3 * L.ngroup);
+  for (int64_t g = 0; g < L.ngroup; g++) {
+    meta[3 * g] = L.goff[g];
+    meta[3 * g + 1] = L.gld[g];
+    meta[3 * g + 2] = L.n - L.r0(g * L.merge);
+  }
+  cudaError_t e = cudaMemcpyAsync(w.gmeta, meta.data(), sizeof(int64_t) * meta.size(), cudaMemcpyHostToDevice, st);
+  if (e) return e;
+  return cudaStreamSynchronize(st);   // `meta` is a host temporary
+}
+
+// all groups: Gram and merged T (depends only on the full->band output: the solve driver
+// runs it on an auxiliary stream, concurrently with the tridiagonal solve)
+cudaError_t bt1_prep(const F2BLayout& L, const double* vstore, const double* Tpanel, BT1Work& w, cudaStream_t st) {
+  if (L.ngroup == 0) return cudaSuccess;
+  const int K = L.merge * L.b;
+  KScope ks(KC_BT1_PREP, st, 2);
+  using TG = GemmTile<64, 64, 16, 32, 32, 2, true, false>;
+  bt1_gram_kernel<<<dim3(K / 64, K / 64, (unsigned)L.ngroup), 128, TG::SMEM_BYTES, st>>>(vstore, w.gmeta, K, w.G);
+  bt1_tmerge_kernel<<<(unsigned)L.ngroup, 256, 0, st>>>(w.G, Tpanel, L.npanel, L.merge, L.b, w.T, w.Y);
+  return cudaGetLastError();
+}
+
 cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,
                     int64_t ldx, int64_t ncols, BT1Work& w, cudaStream_t st) {
-  (void)tau_all;
+  cudaError_t e = bt1_upload_meta(L, w, st);
+  if (e) return e;
+  e = bt1_prep(L, vstore, Tpanel, w, st);
+  if (e) return e;
+  return bt1_apply(L, vstore, tau_all, Tpanel, X, ldx, ncols, w, st);
+}
+
+cudaError_t bt1_apply(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,
+                      int64_t ldx, int64_t ncols, BT1Work& w, cudaStream_t st) {
+  (void)tau_all; (void)Tpanel;
   cudaError_t e;
   const int b = L.b;
   const int K = L.merge * b;
   if (L.ngroup == 0) return cudaSuccess;
-  {   // all groups: Gram and merged T
-    std::vector<int64_t> meta(3 * L.ngroup);
-    for (int64_t g = 0; g < L.ngroup; g++) {
-      meta[3 * g] = L.goff[g];
-      meta[3 * g + 1] = L.gld[g];
-      meta[3 * g + 2] = L.n - L.r0(g * L.merge);
-    }
-    e = cudaMemcpyAsync(w.gmeta, meta.data(), sizeof(int64_t) * meta.size(), cudaMemcpyHostToDevice, st);
-    if (e) return e;
-    e = cudaStreamSynchronize(st);   // `meta` is a host temporary
-    if (e) return e;
-    KScope ks(KC_BT1_PREP, st, 2);
-    using TG = GemmTile<64, 64, 16, 32, 32, 2, true, false>;
-    bt1_gram_kernel<<<dim3(K / 64, K / 64, (unsigned)L.ngroup), 128, TG::SMEM_BYTES, st>>>(vstore, w.gmeta, K, w.G);
-    bt1_tmerge_kernel<<<(unsigned)L.ngroup, 256, 0, st>>>(w.G, Tpanel, L.npanel, L.merge, b, w.T, w.Y);
-  }
   for (int64_t g = L.ngroup - 1; g >= 0; g--) {
     const int64_t r0 = L.r0(g * L.merge);
     const int64_t m = L.n - r0;

@@ -50,6 +50,9 @@ struct Ctx {
   // distributed
   int nranks = 1, rank = 0;
   void* nccl = nullptr;
+  // auxiliary stream: BT1 / BT2 preparation concurrent with the tridiagonal solve
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // Layout of the F2B reflector store: panels grouped by `merge` into block
@@ -196,6 +199,8 @@ cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, 
 void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w);
 cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cudaStream_t st);
 cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st);
+cudaError_t bt2_prep(const B2TLayout& L, B2TWork& w, cudaStream_t st);   // [U | V] of every group
+cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st);
 cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st,
                          int P = 1, int rank = 0);
 cudaError_t band_copy(const double* ABin, int64_t ldin, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st);
@@ -208,6 +213,10 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
 cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st);
 // bt1.cu
 void bt1_reserve(Arena& ar, const F2BLayout& L, int64_t ncols, BT1Work& w);
+cudaError_t bt1_upload_meta(const F2BLayout& L, BT1Work& w, cudaStream_t st);
+cudaError_t bt1_prep(const F2BLayout& L, const double* vstore, const double* Tpanel, BT1Work& w, cudaStream_t st);
+cudaError_t bt1_apply(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,
+                      int64_t ldx, int64_t ncols, BT1Work& w, cudaStream_t st);
 cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,
                     int64_t ldx, int64_t ncols, BT1Work& w, cudaStream_t st);
 cudaError_t split_output(const double* X, int64_t ldx, int64_t n, int64_t nev, double* Zre, double* Zim, int64_t ldz,

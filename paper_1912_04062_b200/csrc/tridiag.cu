@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(128) td_msect_kernel(const double* a2, const i
     const double h = (hi - lo) / (K + 1);
     const double x = lo + h * (k + 1);
     const int c = done ? 0 : (td_sturm32(a2, s0, m, x, pivmin) > i);
-    const unsigned msk = (__ballot_sync(0xffffffffu, c) >> gbase) & ((1u << K) - 1u);
+    const unsigned msk = (__ballot_sync(0xffffffffu, c) >> gbase) & (K == 32 ? 0xffffffffu : ((1u << K) - 1u));
     if (!done) {
       const int f = msk ? __ffs(msk) - 1 : K;   // first point with count > i
       const double nlo = (f > 0) ? lo + h * f : lo;
@@ -748,11 +748,22 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     cudaMemcpyAsync(d_i, ti.data(), sizeof(int64_t) * ntask, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(w.gtask, tg.data(), sizeof(double) * ntask, cudaMemcpyHostToDevice, st);
     {
+      // points per multisection round: as many as keep ~half the device's thread slots busy
+      // (K lanes share one eigenvalue; ~log_{K+1} rounds): 8 for the full spectrum on one
+      // GPU, 16 / 32 for the per-rank slices of the distributed solve
       KScope ks(KC_TRID_BISECT, st);
-      constexpr int K = 8;
-      if (qb > qa)
-        td_msect_kernel<K><<<(unsigned)(((qb - qa) * K + 127) / 128), 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa,
-                                                                                   qb, pivmin, w.lamc);
+      int nsm = 148, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t slots = (int64_t)nsm * 1024, nt = qb - qa;
+      int K = (nt * 32 <= slots) ? 32 : (nt * 16 <= slots) ? 16 : 8;
+      if (const char* v = getenv("SKEWEIG_MSECT_K")) K = atoi(v) == 32 ? 32 : atoi(v) == 16 ? 16 : 8;   // experiments
+      if (nt > 0) {
+        const unsigned grid = (unsigned)((nt * K + 127) / 128);
+        if (K == 32) td_msect_kernel<32><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc);
+        else if (K == 16) td_msect_kernel<16><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc);
+        else td_msect_kernel<8><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc);
+      }
     }
     if (P > 1) {
       ncclResult_t r = ncclAllGather(w.lamc + qa, w.lamc, (size_t)cnt, ncclDouble, (ncclComm_t)d->comm, st);
