@@ -389,13 +389,15 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
     for (int u = 0; u < 4; u++) {
       rr[u] = k + 1 + ti + 16 * u;
       cc[u] = k + 1 + tj + 16 * u;
-      xr[u] = xrow[(rr[u] < KB ? rr[u] : KB - 1) * xs];
-      yc[u] = yrow[cc[u] < KB ? cc[u] : KB - 1];
+      xr[u] = rr[u] < KB ? xrow[rr[u] * xs] : 0.0;
+      yc[u] = cc[u] < KB ? yrow[cc[u]] : 0.0;
     }
+    // only the live trailing part is read (the block shrinks with k)
 #pragma unroll
     for (int u = 0; u < 4; u++)
 #pragma unroll
-      for (int v = 0; v < 4; v++) m[u][v] = Ms[(rr[u] < KB ? rr[u] : KB - 1) * LDK + (cc[v] < KB ? cc[v] : KB - 1)];
+      for (int v = 0; v < 4; v++)
+        m[u][v] = (rr[u] < KB && cc[v] < KB && (!upper || cc[v] >= rr[u])) ? Ms[rr[u] * LDK + cc[v]] : 0.0;
     __syncthreads();   // every read of row/column k and of the tile precedes the writes
 #pragma unroll
     for (int u = 0; u < 4; u++)
