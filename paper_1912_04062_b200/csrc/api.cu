@@ -145,11 +145,11 @@ int skew_ctx_create(skew_ctx* out, int device, void* cuda_stream) {
   ctx->c.num_sms = nsm;
   ctx->c.prm.b = env_int("SKEWEIG_B", 64);
   ctx->c.prm.bt2_k = env_int("SKEWEIG_BT2_K", 32);
-  ctx->c.prm.bt1_merge = env_int("SKEWEIG_BT1_MERGE", 4);
+  ctx->c.prm.bt1_merge = env_int("SKEWEIG_BT1_MERGE", 8);
   ctx->c.prm.reorth_w = env_int("SKEWEIG_REORTH_W", 32);
   if (ctx->c.prm.b < 2 || ctx->c.prm.b > 64 || (ctx->c.prm.b & 1)) ctx->c.prm.b = 64;
   if (ctx->c.prm.bt2_k != 32) ctx->c.prm.bt2_k = 32;
-  if (ctx->c.prm.bt1_merge < 1 || ctx->c.prm.bt1_merge > 8) ctx->c.prm.bt1_merge = 4;
+  if (ctx->c.prm.bt1_merge < 1 || ctx->c.prm.bt1_merge > 8) ctx->c.prm.bt1_merge = 8;
   if (ctx->c.prm.reorth_w < 0 || ctx->c.prm.reorth_w > 256) ctx->c.prm.reorth_w = 32;
   for (int s = 0; s < ST_COUNT; s++) {
     cudaEventCreate(&ctx->ev_start[s]);

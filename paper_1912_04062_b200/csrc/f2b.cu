@@ -379,31 +379,22 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
     grid_barrier(a.gbar, bar_epoch);
     TS();
   };
-  // CTA 0: kb x kb rank-1 trailing update Ms[r][c] -= x_r y_c over rows/cols > k (c >= r
-  // if upper): 16 x 16 threads, each a 4 x 4 register block, all loads before the stores
-  const int ti = tid >> 4, tj = tid & 15;
-  auto rank1 = [&](int k, const double* xrow, int xs, const double* yrow, bool upper) {
-    double xr[4], yc[4], m[4][4];
-    int rr[4], cc[4];
+  const int ti = tid >> 4, tj = tid & 15;   // CTA 0's 16 x 16 thread grid over kb x kb tiles
+  // CTA 0: Ms[r][c] -= (s * xrow[r*xs]) * yrow[c] over r, c > k (c >= r if upper), the
+  // thread's own 4 x 4 block only; row / column k are not written in the same step, so the
+  // caller needs ONE barrier per step (after this)
+  auto rank1_own = [&](int k, const double* xrow, int xs, double xscale, const double* yrow, bool upper) {
 #pragma unroll
     for (int u = 0; u < 4; u++) {
-      rr[u] = k + 1 + ti + 16 * u;
-      cc[u] = k + 1 + tj + 16 * u;
-      xr[u] = rr[u] < KB ? xrow[rr[u] * xs] : 0.0;
-      yc[u] = cc[u] < KB ? yrow[cc[u]] : 0.0;
+      const int r = k + 1 + ti + 16 * u;
+      if (r >= KB) continue;
+      const double x = xrow[r * xs] * xscale;
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int c = k + 1 + tj + 16 * v;
+        if (c < KB && (!upper || c >= r)) Ms[r * LDK + c] -= x * yrow[c];
+      }
     }
-    // only the live trailing part is read (the block shrinks with k)
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-#pragma unroll
-      for (int v = 0; v < 4; v++)
-        m[u][v] = (rr[u] < KB && cc[v] < KB && (!upper || cc[v] >= rr[u])) ? Ms[rr[u] * LDK + cc[v]] : 0.0;
-    __syncthreads();   // every read of row/column k and of the tile precedes the writes
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-#pragma unroll
-      for (int v = 0; v < 4; v++)
-        if (rr[u] < KB && cc[v] < KB && (!upper || cc[v] >= rr[u])) Ms[rr[u] * LDK + cc[v]] = m[u][v] - xr[u] * yc[v];
   };
   // CTA 0: upper Cholesky G = R^T R in Ms (row-major r*LDK + c); returns ok
   __shared__ int bad;
@@ -418,19 +409,19 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
       if (lane == 0) { gmax = gm; bad = 0; }
     }
     __syncthreads();
+    // right-looking, one barrier per step: row k of R goes to Ms2 (Ms row k is read-only in
+    // step k), the trailing update uses R[k][r] R[k][c] = G'[k][r] G'[k][c] / d
     for (int k = 0; k < KB; k++) {
       const double d = Ms[k * LDK + k];
       const double rkk = (d > 0.0) ? sqrt(d) : 1.0, inv = 1.0 / rkk;
-      __syncthreads();
       if (tid == 0 && !(d > 1e-12 * gmax)) bad = 1;
-      if (tid >= k && tid < KB) Ms[k * LDK + tid] = (tid == k) ? rkk : Ms[k * LDK + tid] * inv;
-      __syncthreads();
-      rank1(k, Ms + k * LDK, 1, Ms + k * LDK, true);   // x_r = R[k][r], y_c = R[k][c]
+      if (tid >= k && tid < KB) Ms2[k * LDK + tid] = (tid == k) ? rkk : Ms[k * LDK + tid] * inv;
+      rank1_own(k, Ms + k * LDK, 1, inv * inv, Ms + k * LDK, true);
       __syncthreads();
     }
     for (int e = tid; e < KB * KB; e += blockDim.x) {
       const int r = e / KB, c = e % KB;
-      if (c < r) Ms[r * LDK + c] = 0.0;
+      Ms[r * LDK + c] = (c >= r) ? Ms2[r * LDK + c] : 0.0;
     }
     __syncthreads();
     return bad == 0;
@@ -508,17 +499,22 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
     // modified LU of Q1 - S (Q1 = top kb x kb of Q) in Ms (row-major)
     for (int e = tid; e < KB * KB; e += blockDim.x) Ms[(e / KB) * LDK + e % KB] = P(e / KB, e % KB);
     __syncthreads();
+    // one barrier per step: the pivot and L column k go to Ms2 (column k / row k of Ms are
+    // read-only in step k), then merged back into Ms
     for (int k = 0; k < KB; k++) {
       const double d = Ms[k * LDK + k];
       const double sg = (d >= 0.0) ? -1.0 : 1.0;   // S_kk = -sign(d): pivot d - S_kk, |.| >= 1
       const double piv = d - sg, inv = 1.0 / piv;
-      __syncthreads();
-      if (tid == 0) { aux[k] = sg; Ms[k * LDK + k] = piv; }
-      if (tid > k && tid < KB) Ms[tid * LDK + k] *= inv;   // L column
-      __syncthreads();
-      rank1(k, Ms + k, LDK, Ms + k * LDK, false);   // x_r = L[r][k], y_c = U[k][c]
+      if (tid == 0) { aux[k] = sg; Ms2[k * LDK + k] = piv; }
+      if (tid > k && tid < KB) Ms2[tid * LDK + k] = Ms[tid * LDK + k] * inv;   // L column
+      rank1_own(k, Ms + k, LDK, inv, Ms + k * LDK, false);   // x_r = L[r][k], y_c = U[k][c]
       __syncthreads();
     }
+    for (int e = tid; e < KB * KB; e += blockDim.x) {
+      const int r = e / KB, c = e % KB;
+      if (c <= r) Ms[r * LDK + c] = Ms2[r * LDK + c];   // L (strict lower) and the pivots
+    }
+    __syncthreads();
     for (int e = tid; e < KB * KB; e += blockDim.x) {
       const int r = e / KB, c = e % KB;
       gU[e] = (c >= r) ? Ms[r * LDK + c] : 0.0;   // U row-major

@@ -28,7 +28,7 @@ struct Arena {
 struct Params {
   int b = 64;            // band width (F2B panel width), SKEWEIG_B
   int bt2_k = 32;        // BT2 group width (sweeps per group), SKEWEIG_BT2_K
-  int bt1_merge = 4;     // F2B panels merged per BT1 block reflector, SKEWEIG_BT1_MERGE
+  int bt1_merge = 8;     // F2B panels merged per BT1 block reflector, SKEWEIG_BT1_MERGE
   int reorth_w = 32;     // inverse-iteration reorthogonalisation window, SKEWEIG_REORTH_W
   uint64_t seed = 1;     // inverse-iteration start-vector seed
 };

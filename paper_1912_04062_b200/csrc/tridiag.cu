@@ -215,24 +215,36 @@ __global__ void __launch_bounds__(128) td_inverse_kernel(InvArgs a) {
           dd[u] = (k + 2 < m) ? AT(D, k) : 0.0;
         }
       }
+      // reciprocals of the pivots off the dependency chain (loaded with the chunk): the
+      // common case (|a_k| >= 1, or no overflow risk) multiplies; the dlagts perturbation
+      // loop only runs when the pivot is tiny
+      double ra[IU];
+#pragma unroll
+      for (int u = 0; u < IU; u++) ra[u] = (k0 - u >= 0 && aa[u] != 0.0) ? 1.0 / aa[u] : 0.0;
 #pragma unroll
       for (int u = 0; u < IU; u++) {
         const int64_t k = k0 - u;
         if (k >= 0) {
           double temp = yy[u] - bb[u] * y1 - dd[u] * y2;
           double ak = aa[u];
-          double pert = copysign(tol, ak);
-          for (int guard = 0; guard < 2100; guard++) {
-            double absak = fabs(ak);
-            if (absak < 1.0) {
-              if (absak < sfmin) {
-                if (absak == 0.0 || fabs(temp) * sfmin > absak) { ak += pert; pert *= 2.0; continue; }
-                temp *= bignum; ak *= bignum;
-              } else if (fabs(temp) > absak * bignum) { ak += pert; pert *= 2.0; continue; }
+          const double absa = fabs(ak);
+          double yk;
+          if (absa >= 1.0 || (absa >= sfmin && !(fabs(temp) > absa * bignum))) {
+            yk = temp * ra[u];
+          } else {
+            double pert = copysign(tol, ak);
+            for (int guard = 0; guard < 2100; guard++) {
+              double absak = fabs(ak);
+              if (absak < 1.0) {
+                if (absak < sfmin) {
+                  if (absak == 0.0 || fabs(temp) * sfmin > absak) { ak += pert; pert *= 2.0; continue; }
+                  temp *= bignum; ak *= bignum;
+                } else if (fabs(temp) > absak * bignum) { ak += pert; pert *= 2.0; continue; }
+              }
+              break;
             }
-            break;
+            yk = temp / ak;
           }
-          const double yk = temp / ak;
           AT(y, k) = yk;
           y2 = y1; y1 = yk;
           const double ay = fabs(yk);
@@ -748,15 +760,23 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     cudaMemcpyAsync(d_i, ti.data(), sizeof(int64_t) * ntask, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(w.gtask, tg.data(), sizeof(double) * ntask, cudaMemcpyHostToDevice, st);
     {
-      // points per multisection round: as many as keep ~half the device's thread slots busy
-      // (K lanes share one eigenvalue; ~log_{K+1} rounds): 8 for the full spectrum on one
-      // GPU, 16 / 32 for the per-rank slices of the distributed solve
+      // points per multisection round (K lanes share one eigenvalue, ~log_{K+1}(2/eps)
+      // rounds): minimise rounds(K) * max(latency, throughput) of one round -- the Sturm
+      // chain is ~50 dependent cycles per row, the issue cost ~20 warp-instructions per row
+      // and point, spread over nsm x 4 schedulers x 32 lanes (measured: the full spectrum on
+      // one GPU and the per-rank slices at 2 / 4 GPUs prefer K = 8, smaller slices 16)
       KScope ks(KC_TRID_BISECT, st);
       int nsm = 148, dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      const int64_t slots = (int64_t)nsm * 1024, nt = qb - qa;
-      int K = (nt * 32 <= slots) ? 32 : (nt * 16 <= slots) ? 16 : 8;
+      const int64_t nt = qb - qa;
+      int K = 8;
+      double bestc = 1e300;
+      for (int k : {8, 16, 32}) {
+        const double lat = 50.0, thr = 20.0 * (double)nt * k / ((double)nsm * 128.0);
+        const double c = (1.0 / std::log(k + 1.0)) * std::max(lat, thr);
+        if (c < bestc * 0.999) { bestc = c; K = k; }
+      }
       if (const char* v = getenv("SKEWEIG_MSECT_K")) K = atoi(v) == 32 ? 32 : atoi(v) == 16 ? 16 : 8;   // experiments
       if (nt > 0) {
         const unsigned grid = (unsigned)((nt * K + 127) / 128);
