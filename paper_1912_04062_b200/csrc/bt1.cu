@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128) bt1_gram_kernel(const double* vstore, con
 // reduction) and the Gram: block column q of the forward recurrence is
 //   T[0:qb, q] = -T[0:qb, 0:qb] (V_{0:q}^T V_q) T_q,   T[q, q] = T_q
 // (Schreiber-Van Loan).  One CTA per group; operands through L1/L2.
-__global__ void __launch_bounds__(256) bt1_tmerge_kernel(const double* G, const double* Tpanel, int64_t npanel,
+__global__ void __launch_bounds__(1024) bt1_tmerge_kernel(const double* G, const double* Tpanel, int64_t npanel,
                                                          int merge, int b, double* Tm, double* Y) {
   const int64_t g = blockIdx.x;
   const int K = merge * b;
@@ -127,7 +127,7 @@ cudaError_t bt1_prep(const F2BLayout& L, const double* vstore, const double* Tpa
   KScope ks(KC_BT1_PREP, st, 2);
   using TG = GemmTile<64, 64, 16, 32, 32, 2, true, false>;
   bt1_gram_kernel<<<dim3(K / 64, K / 64, (unsigned)L.ngroup), 128, TG::SMEM_BYTES, st>>>(vstore, w.gmeta, K, w.G);
-  bt1_tmerge_kernel<<<(unsigned)L.ngroup, 256, 0, st>>>(w.G, Tpanel, L.npanel, L.merge, L.b, w.T, w.Y);
+  bt1_tmerge_kernel<<<(unsigned)L.ngroup, 1024, 0, st>>>(w.G, Tpanel, L.npanel, L.merge, L.b, w.T, w.Y);
   return cudaGetLastError();
 }
 

@@ -316,6 +316,14 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
   double* gflag = gS + KB;
   double* gfin = a.gram + (size_t)G * KB * KB;
   auto P = [&](int li, int c) -> double& { return Ps[(size_t)c * LDP + li]; };
+  // kb x kb tile from global scratch (L2): all 16 loads per thread in flight, then the stores
+  // (a load -> shared-store loop would serialise one L2 round trip per element)
+  static_assert(KB * KB % 256 == 0, "256 threads");
+  constexpr int NPT = KB * KB / 256;
+  auto ldtile = [&](const double* g, double (&v)[NPT]) {
+#pragma unroll
+    for (int i = 0; i < NPT; i++) v[i] = __ldcg(g + tid + 256 * i);
+  };
   int nts = 0;
   auto TS = [&]() { if (ca.dbg && cta < 2 && tid == 0 && nts < 16) ca.dbg[cta * 16 + nts++] = clock64(); };
   TS();
@@ -362,8 +370,17 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
       for (int base = 0; base < per; base += 28) {
         const int e = cta * per + base + le;
         double s = 0.0;
-        if (le < 28 && base + le < per && e < KB * KB)
-          for (int qq = part; qq < G; qq += 9) s += __ldcg(&a.gram[(size_t)qq * KB * KB + e]);
+        if (le < 28 && base + le < per && e < KB * KB) {
+          constexpr int NQ = (kMaxPanelCTA + 8) / 9;   // loads in flight, fixed-order sum
+          double v[NQ];
+#pragma unroll
+          for (int i = 0; i < NQ; i++) {
+            const int qq = part + 9 * i;
+            v[i] = (qq < G) ? __ldcg(&a.gram[(size_t)qq * KB * KB + e]) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < NQ; i++) s += v[i];
+        }
         if (tid < 9 * 28) red9[tid] = s;
         __syncthreads();
         const int e2 = cta * per + base + tid;
@@ -400,7 +417,12 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
   __shared__ int bad;
   __shared__ double gmax;
   auto cholesky = [&]() -> bool {
-    for (int e = tid; e < KB * KB; e += blockDim.x) Ms[(e % KB) * LDK + e / KB] = __ldcg(&gfin[e]);
+    {
+      double v[NPT];
+      ldtile(gfin, v);
+#pragma unroll
+      for (int i = 0; i < NPT; i++) { const int e = tid + 256 * i; Ms[(e % KB) * LDK + e / KB] = v[i]; }
+    }
     __syncthreads();
     if (warp == 0) {
       double gm = fmax(Ms[lane * LDK + lane], Ms[(lane + 32) * LDK + lane + 32]);
@@ -452,7 +474,12 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
   };
   // every CTA: rows of P <- P R^-1 with R (upper) from global, right-looking per row
   auto trsm_rows = [&](const double* gRm) {
-    for (int e = tid; e < KB * KB; e += blockDim.x) Ms2[(e / KB) * LDK + e % KB] = __ldcg(&gRm[e]);   // row-major
+    {
+      double v[NPT];
+      ldtile(gRm, v);
+#pragma unroll
+      for (int i = 0; i < NPT; i++) { const int e = tid + 256 * i; Ms2[(e / KB) * LDK + e % KB] = v[i]; }   // row-major
+    }
     __syncthreads();
     if (tid < KB) aux[tid] = 1.0 / Ms2[tid * LDK + tid];
     __syncthreads();
@@ -468,7 +495,12 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
       if (pass == 0) {
         for (int e = tid; e < KB * KB; e += blockDim.x) gR1[e] = Ms[(e / KB) * LDK + e % KB];
       } else {
-        for (int e = tid; e < KB * KB; e += blockDim.x) Ms2[(e / KB) * LDK + e % KB] = __ldcg(&gR[e]);   // R1
+        {
+          double v[NPT];
+          ldtile(gR, v);
+#pragma unroll
+          for (int i = 0; i < NPT; i++) { const int e = tid + 256 * i; Ms2[(e / KB) * LDK + e % KB] = v[i]; }   // R1
+        }
         __syncthreads();
         for (int e = tid; e < KB * KB; e += blockDim.x) {
           const int r = e / KB, c = e % KB;
@@ -526,7 +558,12 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
   grid_barrier(a.gbar, bar_epoch);
   TS();
   // V: rows >= kb: y = q U^-1 (row solve with U upper, right-looking); rows < kb: L1
-  for (int e = tid; e < KB * KB; e += blockDim.x) Ms2[(e / KB) * LDK + e % KB] = __ldcg(&gU[e]);
+  {
+    double v[NPT];
+    ldtile(gU, v);
+#pragma unroll
+    for (int i = 0; i < NPT; i++) { const int e = tid + 256 * i; Ms2[(e / KB) * LDK + e % KB] = v[i]; }
+  }
   __syncthreads();
   if (tid < KB) aux[KB + tid] = 1.0 / Ms2[tid * LDK + tid];
   __syncthreads();
@@ -544,9 +581,14 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
     __syncthreads();
     double* Ts = Ms2;   // overwrite U copy (no longer needed by CTA 0 after the V rows)
     double* ws = Ps;    // the panel rows are no longer needed either
-    for (int e = tid; e < KB * KB; e += blockDim.x) {
-      const int r = e / KB, c = e % KB;
-      ws[r * LDK + c] = (c >= r) ? -__ldcg(&gU[e]) * aux[c] : 0.0;
+    {
+      double v[NPT];
+      ldtile(gU, v);
+#pragma unroll
+      for (int i = 0; i < NPT; i++) {
+        const int e = tid + 256 * i, r = e / KB, c = e % KB;
+        ws[r * LDK + c] = (c >= r) ? -v[i] * aux[c] : 0.0;
+      }
     }
     __syncthreads();
     // T Y1^T = W column by column: T[:, c] = W[:, c] - sum_{l<c} T[:, l] Y1[c][l]; thread
@@ -562,11 +604,19 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
         __syncthreads();
       }
     }
-    for (int e = tid; e < KB * KB; e += blockDim.x) {
-      const int r = e % KB, c = e / KB;
-      a.T[r + c * a.ldt] = Ts[r * LDK + c];
-      if (r <= c) a.A[SK_IDX(r, c, a.lda)] = aux[r] * __ldcg(&gR[r * KB + c]);
-      else a.A[SK_IDX(r, c, a.lda)] = 0.0;
+    {
+      double v[NPT];   // gR row-major: element (r, c) at r * KB + c
+#pragma unroll
+      for (int i = 0; i < NPT; i++) {
+        const int e = tid + 256 * i, r = e % KB, c = e / KB;
+        v[i] = (r <= c) ? __ldcg(&gR[r * KB + c]) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NPT; i++) {
+        const int e = tid + 256 * i, r = e % KB, c = e / KB;
+        a.T[r + c * a.ldt] = Ts[r * LDK + c];
+        a.A[SK_IDX(r, c, a.lda)] = (r <= c) ? aux[r] * v[i] : 0.0;
+      }
     }
     if (tid < KB) a.tau[tid] = Ts[tid * LDK + tid];
   }
@@ -835,9 +885,19 @@ __global__ void mb_kernel(const double* Z, const double* T, int ldt, int kb, dou
   extern __shared__ double ts[];   // kb x (kb + 1): ts[a * (kb+1) + l] = T[l, a]
   double* zc = ts + kb * (kb + 1);
   const int c = blockIdx.x;
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    const int l = e % kb, a = e / kb;
-    ts[a * (kb + 1) + l] = T[l + (size_t)a * ldt];
+  constexpr int U = 8;   // loads in flight per thread before the shared stores
+  for (int e0 = threadIdx.x; e0 < kb * kb; e0 += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = (e < kb * kb) ? T[(e % kb) + (size_t)(e / kb) * ldt] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int e = e0 + u * blockDim.x;
+      if (e < kb * kb) ts[(e / kb) * (kb + 1) + e % kb] = v[u];
+    }
   }
   for (int l = threadIdx.x; l < kb; l += blockDim.x) zc[l] = Z[l + (size_t)c * kb];
   __syncthreads();
@@ -1058,7 +1118,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     vtx_partial_kernel<16><<<nchunk, 128, TV::SMEM_BYTES, st>>>(Vj, ldv, Wp, ldn, m, kWRows, w.zpart);
     double* Zr = w.zpart + (size_t)nchunk * b * b;
     zsum_kernel<<<(b * b + 255) / 256, 256, 0, st>>>(w.zpart, nchunk, b * b, Zr);
-    mb_kernel<<<b, 64, (size_t)(b * (b + 1) + b) * sizeof(double), st>>>(Zr, Tj, b, b, w.Mb);
+    mb_kernel<<<b, 256, (size_t)(b * (b + 1) + b) * sizeof(double), st>>>(Zr, Tj, b, b, w.Mb);
     GemmArgs ga;
     ga.M = m; ga.N = b; ga.K = b;
     ga.A = Vj; ga.lda = ldv; ga.B = w.Mb; ga.ldb = b; ga.C = Wp; ga.ldc = ldn; ga.alpha = -0.5; ga.beta = 1.0;
