@@ -45,7 +45,22 @@ __device__ __forceinline__ int td_sturm32(const double* __restrict__ a2, int64_t
   if (fabs(q) < pivmin) q = -pivmin;
   cnt += (q < 0);
   const double* p = a2 + s0;
-  for (int k = 1; k < m; k++) {
+  // the a2 loads never depend on the chain: issue 16 of them ahead of each 16 steps, so the
+  // step cost is the division chain, not one L2 round trip per row
+  constexpr int U = 16;
+  int k = 1;
+  for (; k + U <= m; k += U) {
+    double av[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) av[u] = __ldg(p + k - 1 + u);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      q = -sigma - av[u] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += (q < 0);
+    }
+  }
+  for (; k < m; k++) {
     q = -sigma - __ldg(p + k - 1) / q;
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += (q < 0);
@@ -126,10 +141,18 @@ __global__ void __launch_bounds__(128) td_inverse_kernel(InvArgs a) {
   double tol = 0.0;
   {
     double ak = -lambda, bk = al[0];     // current (k) diagonal and super-diagonal
-    for (int64_t k = 0; k + 1 < m; k++) {
-      const double ck = al[k];
+    // alpha is read 16 rows ahead of the pivoting recurrence (loads off the chain)
+    for (int64_t k0 = 0; k0 + 1 < m; k0 += 16) {
+    double alv[17];
+#pragma unroll
+    for (int u = 0; u < 17; u++) alv[u] = (k0 + u < m - 1) ? al[k0 + u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int64_t k = k0 + u;
+      if (k + 1 >= m) break;
+      const double ck = alv[u];
       const double ak1 = -lambda;
-      const double bk1 = (k + 2 < m) ? al[k + 1] : 0.0;
+      const double bk1 = (k + 2 < m) ? alv[u + 1] : 0.0;
       const double scale1 = fabs(ak) + fabs(bk);
       const double scale2 = fabs(ck) + fabs(ak1) + fabs(bk1);
       const double piv1 = (scale1 == 0.0) ? 0.0 : fabs(ak) / scale1;
@@ -158,6 +181,7 @@ __global__ void __launch_bounds__(128) td_inverse_kernel(InvArgs a) {
       tol = fmax(tol, fmax(fabs(ak), fabs(bk)));
       if (k + 2 < m) tol = fmax(tol, fabs(dk));
       ak = na1; bk = nb1;
+    }
     }
     AT(A_, m - 1) = ak;
     tol = fmax(tol, fabs(ak));
@@ -762,9 +786,9 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     {
       // points per multisection round (K lanes share one eigenvalue, ~log_{K+1}(2/eps)
       // rounds): minimise rounds(K) * max(latency, throughput) of one round -- the Sturm
-      // chain is ~50 dependent cycles per row, the issue cost ~20 warp-instructions per row
-      // and point, spread over nsm x 4 schedulers x 32 lanes (measured: the full spectrum on
-      // one GPU and the per-rank slices at 2 / 4 GPUs prefer K = 8, smaller slices 16)
+      // chain is ~50 dependent cycles per row (division), the issue cost ~48 instructions per
+      // row and point (measured: 16384 x 8 chains of 32768 rows in 5.7 ms per round), spread
+      // over nsm x 4 schedulers x 32 lanes.  K = 8 except for very small slices.
       KScope ks(KC_TRID_BISECT, st);
       int nsm = 148, dev = 0;
       cudaGetDevice(&dev);
@@ -773,7 +797,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
       int K = 8;
       double bestc = 1e300;
       for (int k : {8, 16, 32}) {
-        const double lat = 50.0, thr = 20.0 * (double)nt * k / ((double)nsm * 128.0);
+        const double lat = 50.0, thr = 48.0 * (double)nt * k / ((double)nsm * 128.0);
         const double c = (1.0 / std::log(k + 1.0)) * std::max(lat, thr);
         if (c < bestc * 0.999) { bestc = c; K = k; }
       }
