@@ -200,6 +200,8 @@ int skew_ctx_destroy(skew_ctx ctx) {
     cudaStreamDestroy(ctx->c.aux);
     cudaEventDestroy(ctx->c.ev_fork);
     cudaEventDestroy(ctx->c.ev_join);
+    cudaEventDestroy(ctx->c.ev_la_cols);
+    cudaEventDestroy(ctx->c.ev_la_panel);
   }
   for (int s = 0; s < ST_COUNT; s++) { cudaEventDestroy(ctx->ev_start[s]); cudaEventDestroy(ctx->ev_stop[s]); }
   delete ctx;
@@ -280,15 +282,22 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   const int64_t n = p.n;
   const bool vec = (Zre != nullptr);
   if (vec && p.f2b.npanel > 0) CK(bt1_upload_meta(p.f2b, p.b1, st), "bt1 meta");
-  if (vec && !c.aux) {
-    CK(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking), "aux stream");
+  if ((vec || c.nranks > 1) && !c.aux) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);   // hi = greatest priority (the look-ahead panel)
+    CK(cudaStreamCreateWithPriority(&c.aux, cudaStreamNonBlocking, hi), "aux stream");
     CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
     CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
+    CK(cudaEventCreateWithFlags(&c.ev_la_cols, cudaEventDisableTiming), "look-ahead event");
+    CK(cudaEventCreateWithFlags(&c.ev_la_panel, cudaEventDisableTiming), "look-ahead event");
   }
   // ---- full -> band
   tstart(ctx, ST_F2B);
   Dist d;
   d.P = c.nranks; d.rank = c.rank; d.comm = c.nccl;
+  if (d.P > 1 && !getenv("SKEWEIG_NO_LOOKAHEAD")) {   // env: experiments only
+    d.aux = c.aux; d.ev_cols = c.ev_la_cols; d.ev_panel = c.ev_la_panel;
+  }
   if (p.f2b.npanel > 0) {
     CK(cudaMemsetAsync(p.vstore, 0, sizeof(double) * p.f2b.vstore_elems, st), "memset vstore");
     int nerr = 0;

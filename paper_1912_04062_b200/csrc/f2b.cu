@@ -1038,7 +1038,7 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
 }
 
 cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, double* vstore, const F2BWork& w,
-                       cudaStream_t st, const Dist& d, int* nccl_err) {
+                       int nsm, cudaStream_t st, const Dist& d, int* nccl_err) {
   // distributed: trailing column block q (global block j+1+q) is local iff (j+1+q) mod P == rank
   const int qoff = (int)((((int64_t)d.rank - (j + 1)) % d.P + d.P) % d.P);
   const int b = L.b;
@@ -1132,6 +1132,28 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
   ga.M = m; ga.N = m; ga.K = 2 * b;
   ga.A = w.P; ga.lda = ldn; ga.B = w.Q; ga.ldb = ldn; ga.C = S; ga.ldc = lda; ga.alpha = 1.0; ga.beta = 1.0;
   ga.col_stride = d.P; ga.col_off = qoff;   // update only the local column blocks
+  const bool lookahead = d.P > 1 && d.aux && qoff == 0 && j + 1 < L.npanel;   // this rank owns panel j+1
+  if (lookahead) {
+    // look-ahead: column block j+1 (tile column 0) first, then panel j+1 on the aux stream
+    // while this stream updates the remaining local column blocks (disjoint columns)
+    const int64_t ntm = (m + 63) / 64;
+    GemmArgs g0 = ga;
+    g0.col_off = 0; g0.col_stride = (int)(ntm + 1);   // tile column 0 only
+    {
+      KScope ks(KC_R2K, st);
+      e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(g0, st);
+    }
+    if (e) return e;
+    e = cudaEventRecord(d.ev_cols, st);
+    if (e) return e;
+    e = cudaStreamWaitEvent(d.aux, d.ev_cols, 0);
+    if (e) return e;
+    e = f2b_panel(L, j + 1, A, lda, vstore, w, nsm, d.aux);
+    if (e) return e;
+    e = cudaEventRecord(d.ev_panel, d.aux);
+    if (e) return e;
+    ga.col_off = d.P;   // the other local column blocks: tn = P, 2P, ...
+  }
   {
     KScope ks(KC_R2K, st);
     e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
@@ -1153,7 +1175,11 @@ cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, 
   for (int64_t j = 0; j < L.npanel; j++) {
     const int owner = (int)(j % d.P);
     if (d.rank == owner) {
-      e = f2b_panel(L, j, A, lda, vstore, w, nsm, st);
+      if (j > 0 && d.P > 1 && d.aux) {   // factored during step j-1 (look-ahead)
+        e = cudaStreamWaitEvent(st, d.ev_panel, 0);
+      } else {
+        e = f2b_panel(L, j, A, lda, vstore, w, nsm, st);
+      }
       if (e) return e;
     }
     if (d.P > 1) {
@@ -1168,7 +1194,7 @@ cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, 
       ncclResult_t r2 = ncclGroupEnd();
       if (r != ncclSuccess || r2 != ncclSuccess) { *nccl_err = (int)(r != ncclSuccess ? r : r2); return cudaErrorUnknown; }
     }
-    e = f2b_update(L, j, A, lda, vstore, w, st, d, nccl_err);
+    e = f2b_update(L, j, A, lda, vstore, w, nsm, st, d, nccl_err);
     if (e) return e;
   }
   return cudaSuccess;

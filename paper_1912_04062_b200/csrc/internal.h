@@ -53,6 +53,7 @@ struct Ctx {
   // auxiliary stream: BT1 / BT2 preparation concurrent with the tridiagonal solve
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_la_cols = nullptr, ev_la_panel = nullptr;   // full->band look-ahead (distributed)
 };
 
 // Layout of the F2B reflector store: panels grouped by `merge` into block
@@ -188,6 +189,10 @@ struct BT1Work {
 struct Dist {
   int P = 1, rank = 0;
   void* comm = nullptr;   // ncclComm_t
+  // look-ahead (P > 1): the owner of panel j+1 factors it on `aux` (higher priority) while
+  // its main stream finishes the rank-2k update of panel j on the other column blocks
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_cols = nullptr, ev_panel = nullptr;
 };
 
 // f2b.cu

@@ -785,22 +785,15 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     cudaMemcpyAsync(w.gtask, tg.data(), sizeof(double) * ntask, cudaMemcpyHostToDevice, st);
     {
       // points per multisection round (K lanes share one eigenvalue, ~log_{K+1}(2/eps)
-      // rounds): minimise rounds(K) * max(latency, throughput) of one round -- the Sturm
-      // chain is ~50 dependent cycles per row (division), the issue cost ~48 instructions per
-      // row and point (measured: 16384 x 8 chains of 32768 rows in 5.7 ms per round), spread
-      // over nsm x 4 schedulers x 32 lanes.  K = 8 except for very small slices.
+      // rounds): as many as keep about half the device's thread slots busy.  Measured at
+      // n = 32768: one GPU (16384 eigenvalues) K = 8, 95 ms; 4 GPUs (4096 per rank) K = 32,
+      // 62 ms vs K = 8, 98 ms -- the per-round Sturm chain latency dominates small slices.
       KScope ks(KC_TRID_BISECT, st);
       int nsm = 148, dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      const int64_t nt = qb - qa;
-      int K = 8;
-      double bestc = 1e300;
-      for (int k : {8, 16, 32}) {
-        const double lat = 50.0, thr = 48.0 * (double)nt * k / ((double)nsm * 128.0);
-        const double c = (1.0 / std::log(k + 1.0)) * std::max(lat, thr);
-        if (c < bestc * 0.999) { bestc = c; K = k; }
-      }
+      const int64_t slots = (int64_t)nsm * 1024, nt = qb - qa;
+      int K = (nt * 32 <= slots) ? 32 : (nt * 16 <= slots) ? 16 : 8;
       if (const char* v = getenv("SKEWEIG_MSECT_K")) K = atoi(v) == 32 ? 32 : atoi(v) == 16 ? 16 : 8;   // experiments
       if (nt > 0) {
         const unsigned grid = (unsigned)((nt * K + 127) / 128);
