@@ -862,7 +862,9 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     a.scale = w.inv + 5 * stride;
     a.win = w.inv_in; a.seed = prm.seed; a.nfail = w.nfail;
     KScope ks(KC_TRID_INV, st, 2);
-    td_inverse_kernel<8><<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(a);
+    // one warp per CTA: the latency-bound per-vector chains spread over every SM (per-SM
+    // outstanding-load capacity, not the thread count, limits this kernel)
+    td_inverse_kernel<8><<<(unsigned)((nb + 31) / 32), 32, 0, st>>>(a);
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)((nb + 31) / 32));
     td_place_vectors<<<grid, dim3(32, 8), 0, st>>>(a.y, a.scale, nb, c0, w.vblk, w.vblk + nev, n, Q, ldq, c0 - vlo);
   }
