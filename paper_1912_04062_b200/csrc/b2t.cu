@@ -548,7 +548,8 @@ __device__ __forceinline__ void bt2_gemm2(double* Xs, const double* Vs, const do
 template <int NB, int K2, int RW, int RING, int BB>
 __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols, int64_t n,
                                                        const double* __restrict__ UV, const int64_t* __restrict__ gofs,
-                                                       int64_t nblk, long long* dbg) {
+                                                       int64_t nblk, long long* dbg, int nsplit,
+                                                       unsigned long long* prog) {
   using C = BT2Cfg<NB, K2, RW, RING, BB>;
   extern __shared__ __align__(128) double sh[];
   double* Xs = sh;
@@ -557,10 +558,16 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
   uint64_t* full = reinterpret_cast<uint64_t*>(Zs + C::ZS);
   uint64_t* empty = full + 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
-  const int64_t col0 = (int64_t)blockIdx.x * NB;
+  // nsplit CTAs per strip (wavefront): member m takes the sweep blocks nblk-1-m, nblk-1-m-nsplit, ..
+  // Block b only reads rows that block b+1 (the previous member) has written back: a per
+  // producer-warp progress value seq(b)*(n+1) + rows-final orders them (release / acquire).
+  const int member = (int)(blockIdx.x % nsplit);
+  const int64_t strip = blockIdx.x / nsplit;
+  const int64_t col0 = strip * NB;
   const int ncl = (int)smin<int64_t>(NB, ncols - col0);
   const bool vec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-  if (nblk <= 0) return;
+  const int64_t blk0 = nblk - 1 - member;
+  if (nblk <= 0 || blk0 < 0) return;
   for (int e = tid; e < C::XS; e += blockDim.x) Xs[e] = 0.0;   // ring rows beyond n stay finite
   if (tid == 0) {
     mbar_init(&full[0], 128); mbar_init(&full[1], 128);
@@ -622,38 +629,68 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
         bulk_g2s(G0 + b * C::GS, UV + g * C::GS, (unsigned)(C::GS * sizeof(double)), &full[b]);
       }
     };
+    const int64_t pred = strip * nsplit + (member + nsplit - 1) % nsplit;
+    auto wait_rows = [&](int64_t b, int64_t rend) {   // rows < rend of block b's input are final
+      if (nsplit == 1 || nblk - 1 - b < 1) return;
+      const unsigned long long need =
+          (unsigned long long)(nblk - 2 - b) * (unsigned long long)(n + 1) + (unsigned long long)smin<int64_t>(rend, n);
+      if (lane == 0)
+        while (ld_acquire_gpu_u64(prog + pred * 4 + pw) < need) { }
+      __syncwarp();
+    };
+    auto publish = [&](int64_t b, int64_t rend) {      // rows < rend of block b written back
+      if (nsplit == 1) return;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release_gpu_u64(prog + (int64_t)blockIdx.x * 4 + pw,
+                           (unsigned long long)(nblk - 1 - b) * (unsigned long long)(n + 1) +
+                               (unsigned long long)smin<int64_t>(rend, n));
+      }
+    };
     // step 0
-    int64_t blk = nblk - 1, t = 0;
+    int64_t blk = blk0, t = 0;
     int off = 0;
     load_group(gofs[blk], 0);
+    wait_rows(blk, blk * K2 + RW);
     load_rows(blk * K2, RW, 0);
     cp_async_mbar_arrive(&full[0]);
     int64_t pblk = -1, pt = 0;
     int poff = 0;
     bool pstored = true;    // step q-1 already written back
+    int64_t pub_blk = -1, pub_rend = 0;   // rows written back but not yet published
     for (int64_t q = 0;; q++) {
       int64_t nblk_ = blk, nt = t + 1;
       int noff = off + BB;
-      if (nt >= ntask_of(blk)) { nblk_ = blk - 1; nt = 0; noff = off + RW; }
+      if (nt >= ntask_of(blk)) { nblk_ = blk - nsplit; nt = 0; noff = off + RW; }
       if (noff >= RING) noff -= RING;
       const bool has_next = nblk_ >= 0;
       if (!pstored) {   // consumers released step q-1: write back its leaving rows
         mbar_wait(&empty[(q - 1) & 1], (unsigned)(((q - 1) >> 1) & 1));
         const bool pfinal = (pt + 1 >= ntask_of(pblk));
         store_rows(pblk * K2 + pt * BB, pfinal ? RW : BB, poff);
+        // published after this iteration's loads are issued: the publishing fence waits for
+        // the stores, which then overlaps the consumers' step instead of delaying the loads
+        pub_blk = pblk;
+        pub_rend = pblk * K2 + pt * BB + (pfinal ? RW : BB);
       }
       bool stored = false;
-      if (has_next && nblk_ != blk && ntask_of(blk) == 1) {
-        // the next block's first window overlaps this single-step block's window:
-        // wait for step q and write it back before loading
+      if (has_next && nblk_ != blk && (ntask_of(blk) == 1 || nsplit > 1)) {
+        if (pub_blk >= 0) { publish(pub_blk, pub_rend); pub_blk = -1; }
+        // the next block's first window overlaps this single-step block's window -- or, in
+        // the wavefront, the partner CTA needs this block's last rows before it can publish
+        // the rows our next block waits for: wait for step q and write it back before loading
         mbar_wait(&empty[q & 1], (unsigned)((q >> 1) & 1));
         store_rows(blk * K2 + t * BB, RW, off);
+        publish(blk, blk * K2 + t * BB + RW);
         stored = true;
       }
       if (!has_next) {
+        if (pub_blk >= 0) { publish(pub_blk, pub_rend); pub_blk = -1; }
         if (!stored) {
           mbar_wait(&empty[q & 1], (unsigned)((q >> 1) & 1));
           store_rows(blk * K2 + t * BB, RW, off);
+          publish(blk, blk * K2 + t * BB + RW);
         }
         break;
       }
@@ -663,11 +700,15 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
         if (nblk_ == blk) {
           int so = noff + (RW - BB);
           if (so >= RING) so -= RING;
-          load_rows(nblk_ * K2 + nt * BB + (RW - BB), BB, so);
+          const int64_t r0 = nblk_ * K2 + nt * BB + (RW - BB);
+          wait_rows(nblk_, r0 + BB);
+          load_rows(r0, BB, so);
         } else {
+          wait_rows(nblk_, nblk_ * K2 + RW);
           load_rows(nblk_ * K2, RW, noff);
         }
         cp_async_mbar_arrive(&full[b]);
+        if (pub_blk >= 0) { publish(pub_blk, pub_rend); pub_blk = -1; }
       }
       pblk = blk; pt = t; poff = off; pstored = stored;
       blk = nblk_; t = nt; off = noff;
@@ -678,7 +719,7 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
   long long ph[6] = {0, 0, 0, 0, 0, 0}, tprev = 0, nsteps = 0;
   const bool prof = (dbg != nullptr) && blockIdx.x == 0 && threadIdx.x == 0;
 #define BT2_TS(k) do { if (prof) { long long _t = clock64(); ph[k] += _t - tprev; tprev = _t; } } while (0)
-  int64_t blk = nblk - 1, t = 0;
+  int64_t blk = blk0, t = 0;
   int off = 0;
   for (int64_t q = 0;; q++) {
     if (prof) { tprev = clock64(); nsteps++; }
@@ -708,7 +749,7 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
     // advance
     int64_t nt = t + 1;
     int noff = off + BB;
-    if (nt >= ntask_of(blk)) { blk--; nt = 0; noff = off + RW; }
+    if (nt >= ntask_of(blk)) { blk -= nsplit; nt = 0; noff = off + RW; }
     if (noff >= RING) noff -= RING;
     if (blk < 0) break;
     t = nt; off = noff;
@@ -756,6 +797,7 @@ void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w) {
   w.qtau = ar.take<double>((size_t)ng * L.k2);
   if (vectors) w.qT = ar.take<double>((size_t)ng * 2 * L.k2 * (L.b + L.k2 + 4));   // [U | V] per group
   w.gofs = ar.take<int64_t>(std::max<int64_t>(L.nblk, 1));
+  if (vectors) w.prog = ar.take<unsigned long long>((size_t)4 * 2 * ((L.n + 63) / 64 + 1));   // BT2 wavefront flags
 }
 
 static int chase_grid(int64_t n, int b, int nsm, int lag) {
@@ -857,21 +899,35 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
     const double tw = (double)((a64 + nsm - 1) / nsm) + kNB32Cost * (double)((a32 + nsm - 1) / nsm);
     if (tw < best - 1e-9) { best = tw; n64 = a64; }
   }
+  // Wavefront option: all strips 64 wide, each walked by TWO CTAs that take alternate sweep
+  // blocks (the kernel's nsplit; 16-byte aligned X only).  Correct (bit-identical) but not
+  // yet faster than the 64/32 mix: 4096 columns at n = 32768 take 671 ms split vs 589 ms in
+  // 32-wide strips (tools/bt2_time.py), so it is only enabled by SKEWEIG_BT2_SPLIT=2.
+  const bool xvec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  int nsplit = 1;
+  if (const char* v = getenv("SKEWEIG_BT2_SPLIT")) nsplit = (atoi(v) == 2 && xvec && w.prog) ? 2 : 1;   // experiments
+  if (nsplit == 2) n64 = s64;
   if (const char* v = getenv("SKEWEIG_BT2_NB")) n64 = (atoi(v) == 32) ? 0 : s64;   // experiments
+  if (n64 != s64) nsplit = 1;
   const int64_t c64 = std::min<int64_t>(ncols, 64 * n64), c32 = ncols - c64;
-  auto launch = [&](auto kern, size_t smem, int NBv, int64_t cbeg, int64_t cnt) -> cudaError_t {
+  auto launch = [&](auto kern, size_t smem, int NBv, int64_t cbeg, int64_t cnt, int ns) -> cudaError_t {
     if (cnt <= 0) return cudaSuccess;
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2) return e2;
+    const int64_t grid = ((cnt + NBv - 1) / NBv) * ns;
+    if (ns > 1) {
+      e2 = cudaMemsetAsync(w.prog, 0, sizeof(unsigned long long) * 4 * (size_t)grid, st);
+      if (e2) return e2;
+    }
     KScope ks(KC_BT2, st);
-    kern<<<(unsigned)((cnt + NBv - 1) / NBv), 384, smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk,
-                                                               dbgp);
+    kern<<<(unsigned)grid, 384, smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp, ns, w.prog);
     return cudaGetLastError();
   };
-  e = launch(bt2_ws_kernel<64, K2, RW, RING, BB>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64, 0, c64);
+  e = launch(bt2_ws_kernel<64, K2, RW, RING, BB>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64, 0, c64,
+             nsplit);
   if (e) return e;
   e = launch(bt2_ws_kernel<32, K2, RW, RING, BB>, BT2Cfg<32, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 32, c64,
-             c32);
+             c32, 1);
   if (e) return e;
   if (dbgp) {
     long long h[6];

@@ -154,6 +154,7 @@ struct B2TWork {
   double* qtau = nullptr;
   double* qT = nullptr;
   int64_t* gofs = nullptr;
+  unsigned long long* prog = nullptr;   // BT2 wavefront: per CTA x producer warp progress
 };
 
 struct TridWork {

@@ -305,3 +305,32 @@ def test_reorth_paths_random(sk, fused, monkeypatch):
     assert st == 0
     lam, Zre, Zim = sk.skew_eig(_cuda(A))
     _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
+
+
+# ------------------------------------------------------------------ BT2 strip schedules
+@pytest.mark.parametrize("n,ncols", [(700, 192), (2100, 640)])
+def test_bt2_wavefront_split_bitwise(sk, n, ncols, monkeypatch):
+    """BT2 with two CTAs per 64-column strip (alternate sweep blocks, row-progress flags,
+    b2t.cu bt2_ws_kernel nsplit = 2) applies the same groups to every element in the same
+    order as one CTA per strip: the results must be bit-identical, and equal to the 32-wide
+    strips."""
+    b = sk.band_width()
+    g = torch.Generator(device="cpu").manual_seed(n)
+    AB = torch.rand((n, 2 * b + 2), generator=g, dtype=torch.float64) * 2 - 1
+    AB[:, 0] = 0
+    AB[:, b + 1:] = 0
+    for d in range(1, b + 1):
+        AB[n - d:, d] = 0
+    X0 = torch.randn((ncols, n), generator=g, dtype=torch.float64).cuda().t()   # column-major n x ncols
+    out = {}
+    for key, env in (("one", {"SKEWEIG_BT2_SPLIT": "1", "SKEWEIG_BT2_NB": "64"}),
+                     ("two", {"SKEWEIG_BT2_SPLIT": "2", "SKEWEIG_BT2_NB": "64"}),
+                     ("narrow", {"SKEWEIG_BT2_SPLIT": "1", "SKEWEIG_BT2_NB": "32"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        X = X0.clone()
+        sk.band_to_tridiag(AB.cuda().t(), b, X)
+        torch.cuda.synchronize()
+        out[key] = X
+    assert torch.equal(out["one"], out["two"])
+    assert torch.equal(out["one"], out["narrow"])
