@@ -545,12 +545,13 @@ __device__ __forceinline__ void bt2_gemm2(double* Xs, const double* Vs, const do
 // and signals mbarrier "full" (transaction bytes + cp.async completion arrivals).  The
 // ring offset advances by b per step inside a sweep block and by RW at a block boundary,
 // so the next block's first window never overlaps the window being computed.
-template <int NB, int K2, int RW, int RING, int BB>
+template <int NB, int K2, int RW, int RING, int BB, bool SPLIT>
 __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols, int64_t n,
                                                        const double* __restrict__ UV, const int64_t* __restrict__ gofs,
-                                                       int64_t nblk, long long* dbg, int nsplit,
+                                                       int64_t nblk, long long* dbg, int nsplit_arg,
                                                        unsigned long long* prog) {
   using C = BT2Cfg<NB, K2, RW, RING, BB>;
+  const int nsplit = SPLIT ? nsplit_arg : 1;   // compile-time 1 on the default path
   extern __shared__ __align__(128) double sh[];
   double* Xs = sh;
   double* G0 = Xs + C::XS;            // [2][U | V]
@@ -923,11 +924,15 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
     kern<<<(unsigned)grid, 384, smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp, ns, w.prog);
     return cudaGetLastError();
   };
-  e = launch(bt2_ws_kernel<64, K2, RW, RING, BB>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64, 0, c64,
-             nsplit);
+  if (nsplit > 1)
+    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, true>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64, 0,
+               c64, nsplit);
+  else
+    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, false>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64,
+               0, c64, 1);
   if (e) return e;
-  e = launch(bt2_ws_kernel<32, K2, RW, RING, BB>, BT2Cfg<32, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 32, c64,
-             c32, 1);
+  e = launch(bt2_ws_kernel<32, K2, RW, RING, BB, false>, BT2Cfg<32, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 32,
+             c64, c32, 1);
   if (e) return e;
   if (dbgp) {
     long long h[6];
