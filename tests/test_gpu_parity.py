@@ -334,3 +334,20 @@ def test_bt2_wavefront_split_bitwise(sk, n, ncols, monkeypatch):
         out[key] = X
     assert torch.equal(out["one"], out["two"])
     assert torch.equal(out["one"], out["narrow"])
+
+
+@pytest.mark.parametrize("n", [1000, 2048])
+def test_skew_eig_vs_cusolver_complex_route(sk, n):
+    """the paper's comparison route (complex Hermitian solver on
+    H = -iA) computed by cuSOLVER zheevd must give the same spectrum,
+    and our vectors must be eigenvectors of H with the same eigenvalues (H z = lam z)."""
+    A = skewgen.random_skew(n, 4242 + n)
+    Ad = _cuda(A)
+    H = (-1j) * Ad.to(torch.complex128)
+    w = torch.flip(torch.linalg.eigvalsh(H), [0])[: n // 2].cpu().numpy()
+    lam, Zre, Zim = sk.skew_eig(Ad, n // 2)
+    nA = np.linalg.norm(A)
+    assert np.max(np.abs(lam.cpu().numpy() - w)) <= 1e-12 * nA
+    Z = torch.complex(Zre, Zim)
+    r = torch.linalg.norm(H @ Z - Z * lam.to(torch.complex128), dim=0).max().item()
+    assert r / (n * nA) <= 1e-13

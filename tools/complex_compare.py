@@ -1,0 +1,98 @@
+"""the paper's central comparison (skew solver vs the complex-Hermitian
+route on the same matrix) reproduced on the B200 box, with cuSOLVER as the complex system.
+
+The paper (Tables 1-2 at P:802-807) compares its real skew solver
+with the complex Hermitian eigensolver applied to H = -iA (same eigenvalues, since A z = i lam z
+<=> H z = lam z).  Here the complex route is torch.linalg.eigh / eigvalsh on complex128, which
+dispatches to cuSOLVER (zheevd) -- a library comparison system, never the product path.  The
+skew side is this repo's C-ABI (skew_eig / skew_eigvals) with the input in HBM, as in bench.py.
+
+"100 %" = every eigenpair: n/2 conjugate pairs from the skew solver (the other half is
+Z-bar, -lam), all n from zheevd.  "50 %" = the top n/2 of the n complex eigenpairs,
+i.e. nev = n/4 pairs for the skew solver; cuSOLVER via torch has no subset driver, so the
+complex side of the 50 % row is the full zheevd time (an upper bound, stated in the output).
+
+python tools/complex_compare.py --n 8192 16384 [--reps 2]
+Prints one JSON line per n."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1912_04062_b200 as sk  # noqa: E402
+import skewgen  # noqa: E402
+
+
+def timed(fn, reps):
+    """Best-of-reps device time (ms) with CUDA events on the current stream."""
+    best, out = None, None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return best, out
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--n", type=int, nargs="+", default=[8192, 16384])
+    p.add_argument("--reps", type=int, default=2)
+    a = p.parse_args()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    # warm cuSOLVER handles / workspace paths outside the timed region
+    torch.linalg.eigh(torch.eye(256, dtype=torch.complex128, device=dev))
+    ctx = sk.Context()
+    for n in a.n:
+        A0 = torch.empty((n, n), dtype=torch.float64, device=dev).t()   # column-major lower
+        skewgen.random_skew_lower_device(A0, n, n, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        L = torch.tril(A0, -1)
+        H = (-1j) * (L - L.t()).to(torch.complex128)                     # Hermitian -iA
+        del L
+        A = torch.empty_like(A0.t()).t()
+
+        def skew(nev, vectors=True):
+            def f():
+                A.copy_(A0)
+                if vectors:
+                    return sk.skew_eig(A, nev, ctx=ctx, overwrite_a=True)
+                return sk.skew_eigvals(A, nev, ctx=ctx)
+            return f
+
+        row = {"n": n, "complex_system": "cuSOLVER zheevd via torch.linalg.eigh (complex128)"}
+        t_sk100, (lam, Zre, Zim) = timed(skew(n // 2), a.reps)
+        del Zre, Zim
+        t_sk50, _ = timed(skew(n // 4), a.reps)
+        t_skv, lamv = timed(skew(n // 2, vectors=False), a.reps)
+        if isinstance(lamv, tuple):
+            lamv = lamv[0]
+        t_c, (w, V) = timed(lambda: torch.linalg.eigh(H), 1)
+        del V
+        t_cv, wv = timed(lambda: torch.linalg.eigvalsh(H), 1)
+        wtop = torch.flip(w, [0])[: n // 2]                               # descending, positive half
+        nA = torch.linalg.norm(H).item()
+        row.update({
+            "skew_all_pairs_s": t_sk100 / 1e3, "skew_half_s": t_sk50 / 1e3,
+            "skew_eigvals_s": t_skv / 1e3,
+            "complex_eigh_s": t_c / 1e3, "complex_eigvalsh_s": t_cv / 1e3,
+            "speedup_100pct": t_c / t_sk100, "speedup_50pct_upper_bound_complex": t_c / t_sk50,
+            "speedup_eigvals": t_cv / t_skv,
+            "max_dlam_over_normA": (lam - wtop).abs().max().item() / nA,
+            "max_dlam_eigvals_over_normA": (lamv[: n // 2] - wtop).abs().max().item() / nA,
+        })
+        print(json.dumps(row), flush=True)
+        del H, w, wv, A, A0
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
