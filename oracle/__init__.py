@@ -205,3 +205,45 @@ def bse_eig(M, nev=None, want_vectors=True, seed=1):
     W = form_W(L)
     lam, Zre, Zim, st = skew_eig(W, nev, want_vectors, seed)
     return lam, Zre, Zim, st, 0, L
+
+
+# ---------------------------------------------------------------------------------------
+# Full BSE H_BS pipeline, plain numpy on top of bse_eig above.
+# ---------------------------------------------------------------------------------------
+def bse_build_M(A, B):
+    """Eq. (10) (PAPER.md:563-570): M = JH = [[Re(A+B), Im(A-B)], [-Im(A+B), Re(A-B)]],
+    2n x 2n real, from A = A^H and B = B^T (n x n complex)."""
+    A = np.asarray(A, dtype=np.complex128)
+    B = np.asarray(B, dtype=np.complex128)
+    P, Mn = A + B, A - B
+    return np.block([[P.real, Mn.imag], [-P.imag, Mn.real]])
+
+
+def bse_Q(n):
+    """Theorem 1: Q = 1/sqrt(2) [[I, -iI], [I, iI]] (2n x 2n, unitary)."""
+    I = np.eye(n)
+    return np.block([[I, -1j * I], [I, 1j * I]]) / np.sqrt(2.0)
+
+
+def bse_backtransform(L, Zre, Zim):
+    """Step 4: x = Q J L z.  With L^T J L z = i lam z and M = L L^T,
+    y = J L z satisfies H y = -J M y ... = -i lam y, so i H y = lam y and, by Theorem 1
+    (Q^H H_BS Q = i H), H_BS (Q y) = lam (Q y).  Returns X (2n x nev complex)."""
+    n2 = L.shape[0]
+    Z = np.asarray(Zre) + 1j * np.asarray(Zim)
+    J = np.block([[np.zeros((n2 // 2, n2 // 2)), np.eye(n2 // 2)],
+                  [-np.eye(n2 // 2), np.zeros((n2 // 2, n2 // 2))]])
+    return bse_Q(n2 // 2) @ (J @ (np.tril(L) @ Z))
+
+
+def bse_hbs_eig(A, B, nev=None, seed=1):
+    """The four steps of PAPER.md:596-606 for H_BS = [[A, B], [-B-bar, -A-bar]] (Eq. 9):
+    M (Eq. 10) -> M = L L^T -> eigenpairs of L^T J L -> x = Q J L z.  Returns
+    (lam (nev, descending positive), X (2n x nev complex), status, pivot)."""
+    M = bse_build_M(A, B)
+    n2 = M.shape[0]
+    nev = n2 // 2 if nev is None else nev
+    lam, Zre, Zim, st, piv, L = bse_eig(M, nev, True, seed)
+    if piv:
+        return None, None, st, piv
+    return lam, bse_backtransform(L, Zre, Zim), st, 0

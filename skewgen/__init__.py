@@ -23,10 +23,10 @@ kernel (``skewgen/skewgen.cu`` -> ``libskewgen.so``) used for large n in
 bench.py. tests/test_generator.py checks them bit for bit.
 """
 from .gen import (splitmix64, uniform_pm1, random_skew, random_skew_lower_colmajor,
-                  skew_toeplitz, planted_skew, bse_spd, J_matrix)
+                  skew_toeplitz, planted_skew, bse_spd, bse_AB, J_matrix)
 
 __all__ = ["splitmix64", "uniform_pm1", "random_skew", "random_skew_lower_colmajor",
-           "skew_toeplitz", "planted_skew", "bse_spd", "J_matrix"]
+           "skew_toeplitz", "planted_skew", "bse_spd", "bse_AB", "J_matrix"]
 
 
 def build_device_lib(force=False):

@@ -105,3 +105,18 @@ def J_matrix(n):
     J[:m, m:] = np.eye(m)
     J[m:, :m] = -np.eye(m)
     return J
+
+
+def bse_AB(n, seed):
+    """Definite BSE blocks (PAPER.md:488-499 structure, Eq. (9) definiteness): A Hermitian,
+    B complex symmetric, n x n complex128.  X, Y, X', Y' are uniform_pm1 draws of four
+    key streams; A = (X + X^H)/(4 sqrt n) + 4 I (with Re/Im from X, X'), B = (Y + Y^T)/(4 sqrt n).
+    ||A - 4I||_2, ||B||_2 <~ 1, so Omega = [[A, B], [B-bar, A-bar]] >= 2 I > 0."""
+    jj, ii = np.meshgrid(np.arange(n), np.arange(n), indexing="xy")
+    R = [uniform_pm1(_keys(seed * 4 + s, n, ii, jj)) for s in range(4)]
+    X = R[0] + 1j * R[1]
+    Y = R[2] + 1j * R[3]
+    s = 4.0 * np.sqrt(n)
+    A = (X + X.conj().T) / s + 4.0 * np.eye(n)
+    B = (Y + Y.T) / s
+    return A, B

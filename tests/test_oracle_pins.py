@@ -474,3 +474,59 @@ def test_bse_random_spectrum_equals_JM():
     ev = np.linalg.eigvals(J @ M)       # purely imaginary, +-i lambda
     ref = np.sort(np.abs(ev.imag))[::-1][0::2][: n // 2]
     np.testing.assert_allclose(lam, ref, rtol=1e-12)
+
+
+# --- full BSE H_BS pipeline --------------------------------------
+def _hbs(A, B):
+    return np.block([[A, B], [-B.conj(), -A.conj()]])
+
+
+@pytest.mark.parametrize("n", [3, 16, 40])
+def test_bse_M_is_similarity_of_omega(n):
+    """Eq. (12): M = -i J Q^H S Omega Q, a formula independent of
+    the block formula Eq. (10) the oracle uses; M symmetric and positive definite."""
+    A, B = skewgen.bse_AB(n, 7 + n)
+    M = oracle.bse_build_M(A, B)
+    Q = oracle.bse_Q(n)
+    S = np.diag(np.r_[np.ones(n), -np.ones(n)])
+    Om = np.block([[A, B], [B.conj(), A.conj()]])
+    J = skewgen.J_matrix(2 * n)
+    M12 = -1j * J @ Q.conj().T @ S @ Om @ Q
+    assert np.abs(M12.imag).max() < 1e-13
+    assert np.allclose(M, M12.real, atol=1e-13, rtol=0)
+    assert np.allclose(M, M.T, atol=0, rtol=0)
+    assert np.linalg.eigvalsh(M).min() > 0
+    # Theorem 1: Q unitary and -i J Q^H S Q = I (PAPER.md:586-589)
+    assert np.allclose(Q.conj().T @ Q, np.eye(2 * n), atol=1e-14)
+    assert np.allclose(-1j * J @ Q.conj().T @ S @ Q, np.eye(2 * n), atol=1e-14)
+
+
+@pytest.mark.parametrize("n", [4, 24, 70])
+def test_bse_hbs_eig_vs_brute_force(n):
+    """Whole pipeline against the definition: eigenvalues of the 2n x 2n H_BS by a general
+    complex eigensolver (real, in +-lam pairs for a definite problem) and
+    H_BS x = lam x for every returned pair; x normalised (Q unitary, L^T-weighted)."""
+    A, B = skewgen.bse_AB(n, 100 + n)
+    H = _hbs(A, B)
+    lam, X, st, piv = oracle.bse_hbs_eig(A, B)
+    assert st == 0 and piv == 0
+    ev = np.linalg.eigvals(H)
+    assert np.abs(ev.imag).max() < 1e-10
+    ref = np.sort(ev.real)[::-1][:n]
+    nH = np.linalg.norm(H)
+    assert np.max(np.abs(lam - ref)) <= 1e-12 * nH
+    r = np.linalg.norm(H @ X - X * lam, axis=0) / np.linalg.norm(X, axis=0)
+    assert r.max() <= 1e-12 * nH
+    # the paired eigenvalue -lam has eigenvector [B-bar x2... ]: the H_BS structure maps
+    # x = [u; v] to [v-bar; u-bar] with eigenvalue -lam (PAPER.md:512-516)
+    Xp = np.vstack([X[n:].conj(), X[:n].conj()])
+    rp = np.linalg.norm(H @ Xp + Xp * lam, axis=0) / np.linalg.norm(Xp, axis=0)
+    assert rp.max() <= 1e-12 * nH
+
+
+def test_bse_hbs_not_definite_reports_pivot():
+    n = 6
+    A, B = skewgen.bse_AB(n, 5)
+    A = A - 10.0 * np.eye(n)
+    lam, X, st, piv = oracle.bse_hbs_eig(A, B)
+    assert lam is None and piv >= 1
