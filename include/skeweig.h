@@ -118,6 +118,28 @@ int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, d
 int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev,
                  double* lambda, double* Zre, double* Zim, int64_t ldz, int64_t* pivot_out);
 
+/* Full BSE H_BS pipeline, step 1 (Eq. (10)):
+ * M = [[Re(A+B), Im(A-B)], [-Im(A+B), Re(A-B)]] for H_BS = [[A, B], [-B-bar, -A-bar]]
+ * (Eq. (9)), A = A^H and B = B^T.  A, B: device, n x n complex128 stored as interleaved
+ * (re, im) doubles, column-major, leading dimensions lda, ldb >= n (in complex elements);
+ * only read, caller-owned.  M: device, 2n x 2n real column-major, ldm >= 2n, fully
+ * written.  Hermitian / symmetric structure is not checked (definiteness is: skew_eig_bse
+ * reports SKEW_ERR_NOT_DEFINITE).  Asynchronous on the context stream.  Returns SKEW_OK
+ * or -k for a bad k-th argument (host pointers are rejected). */
+int skew_bse_build_M(skew_ctx ctx, int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                     double* M, int64_t ldm);
+
+/* Full BSE H_BS pipeline, step 4 (PAPER.md:604-606 with Theorem 1):
+ * x_k = Q J L z_k, Q = [[I, -iI], [I, iI]] / sqrt(2), J = [[0, I], [-I, 0]], so that
+ * H_BS x_k = lambda_k x_k.  L: device, n2 x n2 lower-triangular Cholesky factor (as left
+ * in M by skew_eig_bse; entries above the diagonal are ignored), ldl >= n2, n2 even.
+ * Zre/Zim: device, n2 x nev (ldz >= n2), the skew_eig_bse eigenvectors.  X: device,
+ * n2 x nev complex128 interleaved, ldx >= n2 (complex elements), fully written.  Uses
+ * 16 n2 nev bytes of stream-ordered scratch (cudaMallocAsync).  Asynchronous on the
+ * context stream.  Returns SKEW_OK or -k for a bad k-th argument. */
+int skew_bse_backtransform(skew_ctx ctx, int64_t n2, const double* L, int64_t ldl, int64_t nev,
+                           const double* Zre, const double* Zim, int64_t ldz, double* X, int64_t ldx);
+
 /* Per-stage device times (ms) of the last solve, measured with CUDA events on the
  * context stream: [0] full->band, [1] band->tridiagonal, [2] tridiagonal solve,
  * [3] back-transform 2 (bulge reflectors), [4] back-transform 1 (block

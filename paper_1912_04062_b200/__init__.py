@@ -16,7 +16,7 @@ column-major layout the C-ABI takes).
 import ctypes
 import os
 
-__all__ = ["lib", "Context", "skew_eig", "skew_eig_range", "skew_eig_host_range", "skew_eigvals", "skew_eig_bse", "skew_eig_host",
+__all__ = ["lib", "Context", "skew_eig", "skew_eig_range", "skew_eig_host_range", "skew_eigvals", "skew_eig_bse", "bse_hbs_eig", "skew_eig_host",
            "reduce_to_band", "band_to_tridiag", "tridiag_eig", "expand_half_spectrum", "SkewError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -45,6 +45,8 @@ EXPORTS = {
     "skew_eigvals": ([_vp, _i64, _dp, _i64, _i64, _dp], ctypes.c_int),
     "skew_eig_range": ([_vp, _i64, _dp, _i64, _i64, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
     "skew_eig_bse": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64, ctypes.POINTER(_i64)], ctypes.c_int),
+    "skew_bse_build_M": ([_vp, _i64, _dp, _i64, _dp, _i64, _dp, _i64], ctypes.c_int),
+    "skew_bse_backtransform": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _i64, _dp, _i64], ctypes.c_int),
     "skew_stage_times": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int], ctypes.c_int),
     "skew_last_nfail": ([_vp], _i64),
     "skew_status_string": ([ctypes.c_int], ctypes.c_char_p),
@@ -260,7 +262,7 @@ def skew_eigvals(A, nev=None, ctx=None):
     return lam[:nev]
 
 
-def skew_eig_bse(M, nev=None, ctx=None, want_vectors=True):
+def skew_eig_bse(M, nev=None, ctx=None, want_vectors=True, overwrite_m=False):
     """BSE form: SPD M (n x n, n even) -> Cholesky M = L L^T ->
     W = L^T J L -> (lam, Zre, Zim) of the skew W (as skew_eig).  Raises SkewError with
     .status == 4 and .pivot when M is not numerically definite."""
@@ -268,7 +270,7 @@ def skew_eig_bse(M, nev=None, ctx=None, want_vectors=True):
     c = _ctx(ctx)
     n = M.shape[0]
     nev = n // 2 if nev is None else nev
-    Mc = _colmajor(torch, M.to(device=c.device, dtype=torch.float64))
+    Mc = M if (overwrite_m and M.stride(0) == 1) else _colmajor(torch, M.to(device=c.device, dtype=torch.float64))
     c.ensure_workspace(n, nev, (SKEW_WS_VECTORS if want_vectors else 0) | SKEW_WS_BSE)
     lam = torch.empty(max(nev, 1), dtype=torch.float64, device=c.device)
     Zre = _new_colmajor(torch, n, max(nev, 1), c.device) if want_vectors else None
@@ -285,6 +287,28 @@ def skew_eig_bse(M, nev=None, ctx=None, want_vectors=True):
     if want_vectors:
         return lam[:nev], Zre[:, :nev], Zim[:, :nev]
     return lam[:nev]
+
+
+def bse_hbs_eig(A, B, nev=None, ctx=None):
+    """Full BSE pipeline for H_BS = [[A, B], [-B-bar, -A-bar]] (Eq. 9),
+    A = A^H, B = B^T (n x n complex128): skew_bse_build_M (Eq. 10) -> skew_eig_bse
+    (M = L L^T, eigenpairs of L^T J L; M is overwritten by L) -> skew_bse_backtransform
+    (x = Q J L z, Theorem 1).  Returns (lam (nev,) descending positive, X (2n x nev complex128))
+    with H_BS x_k = lam_k x_k.  nev defaults to n (the whole positive half)."""
+    torch = _torch()
+    c = _ctx(ctx)
+    n = A.shape[0]
+    nev = n if nev is None else nev
+    Ac = A.to(device=c.device, dtype=torch.complex128).t().contiguous().t()   # column-major
+    Bc = B.to(device=c.device, dtype=torch.complex128).t().contiguous().t()
+    M = _new_colmajor(torch, 2 * n, 2 * n, c.device)
+    c._check(lib().skew_bse_build_M(c.h, n, _dp(Ac.data_ptr()), Ac.stride(1), _dp(Bc.data_ptr()), Bc.stride(1),
+                                    _dp(M.data_ptr()), M.stride(1)))
+    lam, Zre, Zim = skew_eig_bse(M, nev, ctx=c, overwrite_m=True)   # M now holds L
+    X = torch.empty((nev, 2 * n), dtype=torch.complex128, device=c.device).t()
+    c._check(lib().skew_bse_backtransform(c.h, 2 * n, _dp(M.data_ptr()), M.stride(1), nev, _dp(Zre.data_ptr()),
+                                          _dp(Zim.data_ptr()), Zre.stride(1), _dp(X.data_ptr()), X.stride(1)))
+    return lam, X
 
 
 def skew_eig_host(A_host, nev, lam_host, Zre_host, Zim_host, ctx=None):

@@ -472,6 +472,45 @@ int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, d
 }
 
 // ------------------------------------------------------------------------------------
+// Full H_BS pipeline stages (steps 1 and 4 of PAPER.md:596-606; step 2-3 = skew_eig_bse)
+int skew_bse_build_M(skew_ctx ctx, int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb, double* M,
+                     int64_t ldm) {
+  if (!ctx) return -1;
+  if (n < 1) return -2;
+  if (!A || !is_device_ptr(A)) return -3;
+  if (lda < n) return -4;
+  if (!B || !is_device_ptr(B)) return -5;
+  if (ldb < n) return -6;
+  if (!M || !is_device_ptr(M)) return -7;
+  if (ldm < 2 * n) return -8;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  CK(bse_build_M(A, lda, B, ldb, n, M, ldm, ctx->c.stream), "bse build M");
+  return SKEW_OK;
+}
+
+int skew_bse_backtransform(skew_ctx ctx, int64_t n2, const double* L, int64_t ldl, int64_t nev, const double* Zre,
+                           const double* Zim, int64_t ldz, double* X, int64_t ldx) {
+  if (!ctx) return -1;
+  if (n2 < 2 || (n2 & 1)) return -2;
+  if (!L || !is_device_ptr(L)) return -3;
+  if (ldl < n2) return -4;
+  if (nev < 0 || nev > n2 / 2) return -5;
+  if (nev == 0) return SKEW_OK;
+  if (!Zre || !Zim || !is_device_ptr(Zre) || !is_device_ptr(Zim)) return -6;
+  if (ldz < n2) return -8;
+  if (!X || !is_device_ptr(X)) return -9;
+  if (ldx < n2) return -10;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  cudaStream_t st = ctx->c.stream;
+  double* Y = nullptr;   // Y = L Z (real and imaginary parts), stream-ordered scratch
+  CK(cudaMallocAsync((void**)&Y, sizeof(double) * (size_t)n2 * nev * 2, st), "bse Y alloc");
+  cudaError_t e = bse_backtransform(L, ldl, n2, Zre, Zim, ldz, nev, Y, Y + (size_t)n2 * nev, n2, X, ldx, st);
+  cudaFreeAsync(Y, st);
+  CK(e, "bse backtransform");
+  return SKEW_OK;
+}
+
+// ------------------------------------------------------------------------------------
 // stage entry points
 int skew_stage_reduce_to_band(skew_ctx ctx, int64_t n, double* A, int64_t lda, double* Vout, int64_t ldv,
                               double* Tout, double* tau_out, int64_t* npanel_out) {

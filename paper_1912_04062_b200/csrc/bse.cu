@@ -152,4 +152,108 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------------------------
+// Full H_BS pipeline stages.
+// Step 1, Eq. (10): M = [[Re(A+B), Im(A-B)], [-Im(A+B), Re(A-B)]].
+// A, B: n x n complex, interleaved (re, im) doubles, column-major; one thread per (i, j),
+// consecutive threads down a column -> coalesced 16-byte loads and 8-byte stores.
+__global__ void bse_build_M_kernel(const double2* __restrict__ A, int64_t lda, const double2* __restrict__ B,
+                                   int64_t ldb, int64_t n, double* __restrict__ M, int64_t ldm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (i >= n) return;
+  const double2 a = A[SK_IDX(i, j, lda)], b = B[SK_IDX(i, j, ldb)];
+  M[SK_IDX(i, j, ldm)] = a.x + b.x;            // Re(A+B)
+  M[SK_IDX(i, n + j, ldm)] = a.y - b.y;        // Im(A-B)
+  M[SK_IDX(n + i, j, ldm)] = -(a.y + b.y);     // -Im(A+B)
+  M[SK_IDX(n + i, n + j, ldm)] = a.x - b.x;    // Re(A-B)
+}
+
+cudaError_t bse_build_M(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t n, double* M, int64_t ldm,
+                        cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)n);
+  bse_build_M_kernel<<<grid, 256, 0, st>>>((const double2*)A, lda, (const double2*)B, ldb, n, M, ldm);
+  return cudaGetLastError();
+}
+
+// Step 4, part 1: Y = L Z for lower-triangular L (n2 x n2) and the real
+// and imaginary parts of Z (grid.z = 0 / 1).  64 x 64 output tile per CTA, 256 threads x
+// (4 x 4) FP64 register tile, 16-deep K slabs staged in shared memory; the K loop stops at
+// the tile's last row (L(i, k) = 0 for k > i) and the strictly upper part of the diagonal
+// slab is masked on load.
+static constexpr int kTM = 64, kTK = 16;
+__global__ void __launch_bounds__(256) bse_trmm_kernel(const double* __restrict__ L, int64_t ldl, int64_t n2,
+                                                       const double* __restrict__ Zre, const double* __restrict__ Zim,
+                                                       int64_t ldz, int64_t nev, double* __restrict__ Yre,
+                                                       double* __restrict__ Yim, int64_t ldy) {
+  __shared__ double Ls[kTK][kTM + 1];
+  __shared__ double Zs[kTK][kTM + 1];
+  const double* Z = blockIdx.z ? Zim : Zre;
+  double* Y = blockIdx.z ? Yim : Yre;
+  const int64_t i0 = (int64_t)blockIdx.x * kTM, j0 = (int64_t)blockIdx.y * kTM;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double acc[4][4] = {};
+  const int64_t kend = min(n2, i0 + kTM);
+  for (int64_t k0 = 0; k0 < kend; k0 += kTK) {
+    for (int e = threadIdx.x; e < kTK * kTM; e += 256) {
+      const int r = e % kTM, kk = e / kTM;   // L tile: rows i0 + r, column k0 + kk (coalesced down r)
+      const int64_t gi = i0 + r, gk = k0 + kk;
+      Ls[kk][r] = (gi < n2 && gk < n2 && gk <= gi) ? L[SK_IDX(gi, gk, ldl)] : 0.0;
+      const int kz = e % kTK, c = e / kTK;   // Z tile: rows k0 + kz, column j0 + c
+      const int64_t zk = k0 + kz, zc = j0 + c;
+      Zs[kz][c] = (zk < n2 && zc < nev) ? Z[SK_IDX(zk, zc, ldz)] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTK; kk++) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) { a[u] = Ls[kk][tx + 16 * u]; b[u] = Zs[kk][ty + 16 * u]; }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; u++)
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      const int64_t gi = i0 + tx + 16 * u, gj = j0 + ty + 16 * v;
+      if (gi < n2 && gj < nev) Y[SK_IDX(gi, gj, ldy)] = acc[u][v];
+    }
+}
+
+// Step 4, part 2: x = Q J y with J = [[0, I], [-I, 0]] and Q = [[I, -iI], [I, iI]] / sqrt(2)
+// (Theorem 1):  x_top = (y2 + i y1) / sqrt 2,  x_bot = (y2 - i y1) / sqrt 2
+// for y = [y1; y2] (n rows each), written interleaved complex.
+__global__ void bse_qj_kernel(const double* __restrict__ Yre, const double* __restrict__ Yim, int64_t ldy, int64_t n,
+                              double2* __restrict__ X, int64_t ldx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (i >= n) return;
+  const double s = 0.70710678118654752440;
+  const double y1r = Yre[SK_IDX(i, j, ldy)], y1i = Yim[SK_IDX(i, j, ldy)];
+  const double y2r = Yre[SK_IDX(n + i, j, ldy)], y2i = Yim[SK_IDX(n + i, j, ldy)];
+  X[SK_IDX(i, j, ldx)] = make_double2(s * (y2r - y1i), s * (y2i + y1r));
+  X[SK_IDX(n + i, j, ldx)] = make_double2(s * (y2r + y1i), s * (y2i - y1r));
+}
+
+cudaError_t bse_backtransform(const double* L, int64_t ldl, int64_t n2, const double* Zre, const double* Zim,
+                              int64_t ldz, int64_t nev, double* Yre, double* Yim, int64_t ldy, double* X, int64_t ldx,
+                              cudaStream_t st) {
+  if (n2 <= 0 || nev <= 0) return cudaSuccess;
+  dim3 g1((unsigned)((n2 + kTM - 1) / kTM), (unsigned)((nev + kTM - 1) / kTM), 2);
+  bse_trmm_kernel<<<g1, 256, 0, st>>>(L, ldl, n2, Zre, Zim, ldz, nev, Yre, Yim, ldy);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t n = n2 / 2;
+  dim3 g2((unsigned)((n + 255) / 256), (unsigned)nev);
+  bse_qj_kernel<<<g2, 256, 0, st>>>(Yre, Yim, ldy, n, (double2*)X, ldx);
+  return cudaGetLastError();
+}
+
 }  // namespace sk

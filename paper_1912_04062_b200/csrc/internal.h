@@ -230,5 +230,10 @@ cudaError_t split_output(const double* X, int64_t ldx, int64_t n, int64_t nev, d
 // bse.cu
 cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw, double* S, int64_t lds,
                       double* scratch, int64_t* status_d, cudaStream_t st);
+cudaError_t bse_build_M(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t n, double* M, int64_t ldm,
+                        cudaStream_t st);
+cudaError_t bse_backtransform(const double* L, int64_t ldl, int64_t n2, const double* Zre, const double* Zim,
+                              int64_t ldz, int64_t nev, double* Yre, double* Yim, int64_t ldy, double* X, int64_t ldx,
+                              cudaStream_t st);
 
 }  // namespace sk

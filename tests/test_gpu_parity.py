@@ -351,3 +351,35 @@ def test_skew_eig_vs_cusolver_complex_route(sk, n):
     Z = torch.complex(Zre, Zim)
     r = torch.linalg.norm(H @ Z - Z * lam.to(torch.complex128), dim=0).max().item()
     assert r / (n * nA) <= 1e-13
+
+
+@pytest.mark.parametrize("n,nev", [(70, 70), (300, 120), (520, 520)])
+def test_bse_hbs_pipeline_vs_oracle(sk, n, nev):
+    """SURVEY §8(f) NEXT-2, full H_BS pipeline through the C-ABI
+    (skew_bse_build_M -> skew_eig_bse -> skew_bse_backtransform) against oracle.bse_hbs_eig
+    on the same seeded definite (A, B): eigenvalues, H_BS x = lam x, and each x parallel to
+    the oracle's (simple eigenvalues; phase free, R7)."""
+    A, B = skewgen.bse_AB(n, 900 + n)
+    H = np.block([[A, B], [-B.conj(), -A.conj()]])
+    lam_o, X_o, st, piv = oracle.bse_hbs_eig(A, B, nev)
+    lam, X = sk.bse_hbs_eig(torch.from_numpy(A), torch.from_numpy(B), nev)
+    lam, X = lam.cpu().numpy(), X.cpu().numpy()
+    nH = np.linalg.norm(H)
+    assert np.max(np.abs(lam - lam_o)) <= 1e-12 * nH
+    nx = np.linalg.norm(X, axis=0)
+    assert np.max(np.linalg.norm(H @ X - X * lam, axis=0) / nx) <= 1e-12 * nH
+    cos = np.abs(np.sum(X_o.conj() * X, axis=0)) / (nx * np.linalg.norm(X_o, axis=0))
+    assert np.min(cos) >= 1 - 1e-9
+    # the Q J L map preserves the skew solver's normalisation: ||x|| = ||L z||
+    assert np.allclose(nx, np.linalg.norm(X_o, axis=0), rtol=1e-9)
+
+
+def test_bse_stage_bad_arguments(sk):
+    c = sk.Context()
+    L = sk.lib()
+    assert L.skew_bse_build_M(c.h, 0, None, 1, None, 1, None, 2) == -2
+    A = torch.zeros((4, 4), dtype=torch.complex128, device="cuda")
+    M = torch.zeros((8, 8), dtype=torch.float64, device="cuda")
+    assert L.skew_bse_build_M(c.h, 4, A.data_ptr(), 4, A.data_ptr(), 4, M.data_ptr(), 7) == -8
+    assert L.skew_bse_backtransform(c.h, 7, M.data_ptr(), 8, 1, M.data_ptr(), M.data_ptr(), 8,
+                                    A.data_ptr(), 8) == -2

@@ -75,9 +75,16 @@ def main():
         t_skv, lamv = timed(skew(n // 2, vectors=False), a.reps)
         if isinstance(lamv, tuple):
             lamv = lamv[0]
-        t_c, (w, V) = timed(lambda: torch.linalg.eigh(H), 1)
+        try:
+            t_c, (w, V) = timed(lambda: torch.linalg.eigh(H), 1)
+        except RuntimeError as e:   # cusolverDnXsyevd rejects n = 32768 complex (workspace query)
+            row["cusolver_error"] = str(e).splitlines()[0][:160]
+            torch.backends.cuda.preferred_linalg_library("magma")
+            row["complex_system"] = "MAGMA zheevd via torch.linalg.eigh (complex128; cuSOLVER failed)"
+            t_c, (w, V) = timed(lambda: torch.linalg.eigh(H), 1)
         del V
         t_cv, wv = timed(lambda: torch.linalg.eigvalsh(H), 1)
+        torch.backends.cuda.preferred_linalg_library("default")
         wtop = torch.flip(w, [0])[: n // 2]                               # descending, positive half
         nA = torch.linalg.norm(H).item()
         row.update({
