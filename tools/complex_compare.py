@@ -77,14 +77,18 @@ def main():
             lamv = lamv[0]
         try:
             t_c, (w, V) = timed(lambda: torch.linalg.eigh(H), 1)
-        except RuntimeError as e:   # cusolverDnXsyevd rejects n = 32768 complex (workspace query)
+        except RuntimeError as e:
+            # cusolverDnXsyevd_bufferSize rejects n = 32768 complex (INVALID_VALUE, measured);
+            # torch's MAGMA backend segfaults on the same matrix, so it is not tried.
             row["cusolver_error"] = str(e).splitlines()[0][:160]
-            torch.backends.cuda.preferred_linalg_library("magma")
-            row["complex_system"] = "MAGMA zheevd via torch.linalg.eigh (complex128; cuSOLVER failed)"
-            t_c, (w, V) = timed(lambda: torch.linalg.eigh(H), 1)
+            row.update({"skew_all_pairs_s": t_sk100 / 1e3, "skew_half_s": t_sk50 / 1e3,
+                        "skew_eigvals_s": t_skv / 1e3, "complex_eigh_s": None})
+            print(json.dumps(row), flush=True)
+            del H, A, A0
+            torch.cuda.empty_cache()
+            continue
         del V
         t_cv, wv = timed(lambda: torch.linalg.eigvalsh(H), 1)
-        torch.backends.cuda.preferred_linalg_library("default")
         wtop = torch.flip(w, [0])[: n // 2]                               # descending, positive half
         nA = torch.linalg.norm(H).item()
         row.update({
