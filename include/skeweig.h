@@ -19,11 +19,15 @@
  *  - FP64, column-major, 0-based, 64-bit sizes.
  *  - A skew input is read from its STRICTLY LOWER triangle only; the diagonal and
  *    upper triangle are never read.
- *  - Array pointers may be DEVICE pointers (cudaMalloc / torch) or HOST pointers
- *    (pageable or pinned).  The library detects the kind with
- *    cudaPointerGetAttributes; host arrays are staged through the workspace (the
- *    workspace must then be sized with SKEW_WS_HOST_STAGING).  All arrays of one
- *    call must be of the same kind.
+ *  - Array pointers of skew_eig / skew_eig_range / skew_eigvals / skew_eig_bse may be
+ *    DEVICE pointers (cudaMalloc / torch) or HOST pointers (pageable or pinned).  The
+ *    library detects the kind with cudaPointerGetAttributes; host inputs are staged
+ *    through the workspace (the workspace must then be sized with SKEW_WS_HOST_STAGING).
+ *    Zre and Zim must be of the same kind.  The BSE pipeline stages
+ *    (skew_bse_build_M, skew_bse_backtransform) and the stage entry points take device
+ *    pointers only.
+ *  - Non-finite input (a NaN or Inf in the triangle that is read) is an argument error
+ *    (-3, the A or M argument), detected before any reduction starts.
  *  - Ownership: every array belongs to the caller.  A (or M) is INPUT AND
  *    DESTROYED when it is a device array (it receives reflectors and the band;
  *    contents unspecified on return, LAPACK convention); a host A is not modified.
@@ -59,15 +63,19 @@ extern "C" {
 #define SKEW_WS_VECTORS 1          /* eigenvectors requested (else eigenvalues only) */
 #define SKEW_WS_HOST_STAGING 2     /* room to stage host A (n x n) */
 #define SKEW_WS_BSE 4              /* room for the BSE front-end (Cholesky factor) */
+#define SKEW_WS_BSE_BACKTRANSFORM 8 /* room for skew_bse_backtransform's scratch (16 n2 nev bytes) */
+
+/* skew_eig_bse flags */
+#define SKEW_BSE_HAMILTONIAN_Y 1   /* return y = J L z (H y = -i lambda y, H = -J M) instead of z */
 
 typedef struct skew_ctx_s* skew_ctx;
 
 /* Create a context on CUDA device `device` that enqueues on `cuda_stream`
  * (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream; NULL = legacy
- * default stream).  Tunables are read from the environment once here:
- * SKEWEIG_B (band width b, default 64), SKEWEIG_BT2_K (sweeps per BT2 group,
- * default 32), SKEWEIG_BT1_MERGE (panels per BT1 block reflector, default 4),
- * SKEWEIG_REORTH_W (reorthogonalisation window, default 32). */
+ * default stream).  The internal band width is b = 64 (fixed: the panel, bulge-chase and
+ * BT2 kernels are built for it; reading R10).  Tunables are read from the
+ * environment once here: SKEWEIG_BT1_MERGE (panels per BT1 block reflector, 1..8,
+ * default 8), SKEWEIG_REORTH_W (reorthogonalisation window, default 32). */
 int skew_ctx_create(skew_ctx* out, int device, void* cuda_stream);
 int skew_ctx_destroy(skew_ctx ctx);
 
@@ -78,7 +86,7 @@ int skew_ctx_destroy(skew_ctx ctx);
  * distributed by b-wide column blocks (1D block-cyclic, owner of column c = (c/64) mod
  * nranks; NCCL broadcast of each panel's V, T, tau and allreduce of the skew-SYMM
  * products); the band is combined with an allreduce; the eigenvectors
- * are sharded by skew_eig_range (each rank its own [k0, k1)).  Requires SKEWEIG_B = 64.
+ * are sharded by skew_eig_range (each rank its own [k0, k1)).
  * Returns SKEW_ERR_NCCL on communicator failure. */
 int skew_get_unique_id(char id[128]);
 int skew_ctx_create_dist(skew_ctx* out, int device, void* cuda_stream, int nranks, int rank, const char id[128]);
@@ -111,11 +119,19 @@ int skew_eig_range(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev,
 int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda);
 
 /* BSE form (steps 2-3): M (n x n, n even, symmetric positive
- * definite, lower triangle read; destroyed if device) -> M = L L^T (Cholesky) ->
- * W = L^T J L with J = [[0, I], [-I, 0]] -> eigenpairs of the skew W as in
- * skew_eig.  Zre/Zim may be NULL (eigenvalues only).  On a pivot <= n*eps*max_i M_ii
- * returns SKEW_ERR_NOT_DEFINITE with the 1-based pivot index in *pivot_out. */
-int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev,
+ * definite, lower triangle incl. diagonal read) -> M = L L^T (Cholesky) -> W = L^T J L
+ * with J = [[0, I], [-I, 0]] -> eigenpairs of the skew W as in skew_eig.
+ *   M       device: destroyed, receives L (lower triangle, upper zeroed); host: staged
+ *           through the workspace (size it with SKEW_WS_BSE | SKEW_WS_HOST_STAGING), not
+ *           modified
+ *   flags   0, or SKEW_BSE_HAMILTONIAN_Y: Zre/Zim receive y_k = J L z_k instead of z_k
+ *           (H y_k = -i lambda_k y_k for H = -J M; not normalised, ||y_k|| =
+ *           ||L z_k||); needs Zre/Zim
+ *   Zre/Zim both NULL (eigenvalues only) or both non-NULL, same pointer kind
+ * On a pivot <= n*eps*max_i M_ii returns SKEW_ERR_NOT_DEFINITE with the 1-based pivot
+ * index in *pivot_out.  Argument numbers: ctx 1, n 2, M 3, ldm 4,
+ * nev 5, flags 6, lambda 7, Zre 8, Zim 9, ldz 10. */
+int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, int flags,
                  double* lambda, double* Zre, double* Zim, int64_t ldz, int64_t* pivot_out);
 
 /* Full BSE H_BS pipeline, step 1 (Eq. (10)):
@@ -134,9 +150,11 @@ int skew_bse_build_M(skew_ctx ctx, int64_t n, const double* A, int64_t lda, cons
  * H_BS x_k = lambda_k x_k.  L: device, n2 x n2 lower-triangular Cholesky factor (as left
  * in M by skew_eig_bse; entries above the diagonal are ignored), ldl >= n2, n2 even.
  * Zre/Zim: device, n2 x nev (ldz >= n2), the skew_eig_bse eigenvectors.  X: device,
- * n2 x nev complex128 interleaved, ldx >= n2 (complex elements), fully written.  Uses
- * 16 n2 nev bytes of stream-ordered scratch (cudaMallocAsync).  Asynchronous on the
- * context stream.  Returns SKEW_OK or -k for a bad k-th argument. */
+ * n2 x nev complex128 interleaved, ldx >= n2 (complex elements), fully written; each
+ * column is normalised to unit 2-norm (phase free, reading R7).  Scratch
+ * (16 n2 nev + 8 nev bytes) comes from the context workspace: size it with
+ * skew_workspace_size(ctx, n2, nev, SKEW_WS_BSE_BACKTRANSFORM | ...).  Asynchronous on
+ * the context stream.  Returns SKEW_OK, -k for a bad k-th argument or SKEW_ERR_WORKSPACE. */
 int skew_bse_backtransform(skew_ctx ctx, int64_t n2, const double* L, int64_t ldl, int64_t nev,
                            const double* Zre, const double* Zim, int64_t ldz, double* X, int64_t ldx);
 

@@ -238,12 +238,14 @@ def bse_backtransform(L, Zre, Zim):
 
 def bse_hbs_eig(A, B, nev=None, seed=1):
     """The four steps of PAPER.md:596-606 for H_BS = [[A, B], [-B-bar, -A-bar]] (Eq. 9):
-    M (Eq. 10) -> M = L L^T -> eigenpairs of L^T J L -> x = Q J L z.  Returns
-    (lam (nev, descending positive), X (2n x nev complex), status, pivot)."""
+    M (Eq. 10) -> M = L L^T -> eigenpairs of L^T J L -> x = Q J L z, each x normalised to
+    unit 2-norm ("normalizes x_k to unit 2-norm"; phase free, reading R7).
+    Returns (lam (nev, descending positive), X (2n x nev complex), status, pivot)."""
     M = bse_build_M(A, B)
     n2 = M.shape[0]
     nev = n2 // 2 if nev is None else nev
     lam, Zre, Zim, st, piv, L = bse_eig(M, nev, True, seed)
     if piv:
         return None, None, st, piv
-    return lam, bse_backtransform(L, Zre, Zim), st, 0
+    X = bse_backtransform(L, Zre, Zim)
+    return lam, X / np.linalg.norm(X, axis=0), st, 0

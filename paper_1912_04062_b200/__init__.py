@@ -26,6 +26,8 @@ _lib = None
 SKEW_WS_VECTORS = 1
 SKEW_WS_HOST_STAGING = 2
 SKEW_WS_BSE = 4
+SKEW_WS_BSE_BACKTRANSFORM = 8
+SKEW_BSE_HAMILTONIAN_Y = 1
 SKEW_ERR_NOCONV = 1
 SKEW_ERR_NOT_DEFINITE = 4
 
@@ -44,7 +46,8 @@ EXPORTS = {
     "skew_eig": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
     "skew_eigvals": ([_vp, _i64, _dp, _i64, _i64, _dp], ctypes.c_int),
     "skew_eig_range": ([_vp, _i64, _dp, _i64, _i64, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
-    "skew_eig_bse": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64, ctypes.POINTER(_i64)], ctypes.c_int),
+    "skew_eig_bse": ([_vp, _i64, _dp, _i64, _i64, ctypes.c_int, _dp, _dp, _dp, _i64, ctypes.POINTER(_i64)],
+                     ctypes.c_int),
     "skew_bse_build_M": ([_vp, _i64, _dp, _i64, _dp, _i64, _dp, _i64], ctypes.c_int),
     "skew_bse_backtransform": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _i64, _dp, _i64], ctypes.c_int),
     "skew_stage_times": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int], ctypes.c_int),
@@ -262,10 +265,12 @@ def skew_eigvals(A, nev=None, ctx=None):
     return lam[:nev]
 
 
-def skew_eig_bse(M, nev=None, ctx=None, want_vectors=True, overwrite_m=False):
+def skew_eig_bse(M, nev=None, ctx=None, want_vectors=True, overwrite_m=False, hamiltonian_y=False):
     """BSE form: SPD M (n x n, n even) -> Cholesky M = L L^T ->
-    W = L^T J L -> (lam, Zre, Zim) of the skew W (as skew_eig).  Raises SkewError with
-    .status == 4 and .pivot when M is not numerically definite."""
+    W = L^T J L -> (lam, Zre, Zim) of the skew W (as skew_eig).  hamiltonian_y=True
+    (SKEW_BSE_HAMILTONIAN_Y) returns y = J L z instead of z (H y = -i lam y for H = -J M,
+    unnormalised).  Raises SkewError with .status == 4 and .pivot when M is not
+    numerically definite."""
     torch = _torch()
     c = _ctx(ctx)
     n = M.shape[0]
@@ -276,7 +281,8 @@ def skew_eig_bse(M, nev=None, ctx=None, want_vectors=True, overwrite_m=False):
     Zre = _new_colmajor(torch, n, max(nev, 1), c.device) if want_vectors else None
     Zim = _new_colmajor(torch, n, max(nev, 1), c.device) if want_vectors else None
     piv = _i64(0)
-    rc = lib().skew_eig_bse(c.h, n, _dp(Mc.data_ptr()), Mc.stride(1), nev, _dp(lam.data_ptr()),
+    rc = lib().skew_eig_bse(c.h, n, _dp(Mc.data_ptr()), Mc.stride(1), nev,
+                            SKEW_BSE_HAMILTONIAN_Y if hamiltonian_y else 0, _dp(lam.data_ptr()),
                             _dp(Zre.data_ptr()) if want_vectors else None,
                             _dp(Zim.data_ptr()) if want_vectors else None, n, ctypes.byref(piv))
     if rc == SKEW_ERR_NOT_DEFINITE:
@@ -293,8 +299,9 @@ def bse_hbs_eig(A, B, nev=None, ctx=None):
     """Full BSE pipeline for H_BS = [[A, B], [-B-bar, -A-bar]] (Eq. 9),
     A = A^H, B = B^T (n x n complex128): skew_bse_build_M (Eq. 10) -> skew_eig_bse
     (M = L L^T, eigenpairs of L^T J L; M is overwritten by L) -> skew_bse_backtransform
-    (x = Q J L z, Theorem 1).  Returns (lam (nev,) descending positive, X (2n x nev complex128))
-    with H_BS x_k = lam_k x_k.  nev defaults to n (the whole positive half)."""
+    (x = Q J L z, Theorem 1, normalised to unit 2-norm).  Returns (lam (nev,)
+    descending positive, X (2n x nev complex128)) with H_BS x_k = lam_k x_k.  nev defaults
+    to n (the whole positive half)."""
     torch = _torch()
     c = _ctx(ctx)
     n = A.shape[0]
@@ -306,6 +313,7 @@ def bse_hbs_eig(A, B, nev=None, ctx=None):
                                     _dp(M.data_ptr()), M.stride(1)))
     lam, Zre, Zim = skew_eig_bse(M, nev, ctx=c, overwrite_m=True)   # M now holds L
     X = torch.empty((nev, 2 * n), dtype=torch.complex128, device=c.device).t()
+    c.ensure_workspace(2 * n, nev, SKEW_WS_BSE_BACKTRANSFORM)
     c._check(lib().skew_bse_backtransform(c.h, 2 * n, _dp(M.data_ptr()), M.stride(1), nev, _dp(Zre.data_ptr()),
                                           _dp(Zim.data_ptr()), Zre.stride(1), _dp(X.data_ptr()), X.stride(1)))
     return lam, X
@@ -352,12 +360,8 @@ def reduce_to_band(A, ctx=None, want_reflectors=True):
 
 
 def band_width():
-    v = os.environ.get("SKEWEIG_B", "")
-    try:
-        b = int(v) if v else 64
-    except ValueError:
-        b = 64
-    return b if (2 <= b <= 64 and b % 2 == 0) else 64
+    """The library's internal band width b (fixed at 64, include/skeweig.h)."""
+    return 64
 
 
 def band_to_tridiag(AB, b, X=None, ctx=None):

@@ -23,6 +23,7 @@ struct Plan {
   B2TLayout b2t;
   int64_t n = 0, nev = 0, ldn = 0;
   double* Astage = nullptr;    // n x ldn (host staging / BSE W)
+  double* Mstage = nullptr;    // n x ldn (BSE: host M staged; receives L)
   double* S = nullptr;         // BSE m x m
   double* vstore = nullptr;
   F2BWork fw;
@@ -46,6 +47,11 @@ static void plan_layout(Ctx& c, Plan& p, Arena& ar, int64_t n, int64_t nev, int 
   p.b2t.init(n, b, c.prm.bt2_k);
   if (flags & (SKEW_WS_HOST_STAGING | SKEW_WS_BSE)) p.Astage = ar.take<double>((size_t)p.ldn * n);
   if (flags & SKEW_WS_BSE) p.S = ar.take<double>((size_t)std::max<int64_t>(n / 2, 1) * std::max<int64_t>(n / 2, 1));
+  if ((flags & SKEW_WS_BSE) && (flags & SKEW_WS_HOST_STAGING)) p.Mstage = ar.take<double>((size_t)p.ldn * n);
+  if (flags & SKEW_WS_BSE_BACKTRANSFORM) {   // skew_bse_backtransform: Y = L Z (2 planes) + column norms
+    ar.take<double>((size_t)n * 2 * std::max<int64_t>(nev, 1));
+    ar.take<double>((size_t)std::max<int64_t>(nev, 1));
+  }
   p.vstore = ar.take<double>((size_t)std::max<int64_t>(p.f2b.vstore_elems, 1));
   f2b_reserve(ar, p.f2b, c.num_sms, p.fw, c.nranks);
   b2t_reserve(ar, p.b2t, vec, p.bw);
@@ -66,8 +72,7 @@ static bool plan_bind(Ctx& c, Plan& p, int64_t n, int64_t nev, int flags) {
   ar.base = (char*)c.ws;
   ar.size = c.ws_bytes;
   plan_layout(c, p, ar, n, nev, flags);
-  // any null from take() means out of space
-  return ar.off <= ar.size && p.status != nullptr && p.scratch != nullptr;
+  return !ar.fail && ar.off <= ar.size;
 }
 
 static int env_int(const char* name, int def) {
@@ -143,11 +148,10 @@ int skew_ctx_create(skew_ctx* out, int device, void* cuda_stream) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
   ctx->c.num_sms = nsm;
-  ctx->c.prm.b = env_int("SKEWEIG_B", 64);
+  ctx->c.prm.b = 64;   // band width: fixed (the F2B panel, chase and BT2 kernels are built for b = 64)
   ctx->c.prm.bt2_k = env_int("SKEWEIG_BT2_K", 32);
   ctx->c.prm.bt1_merge = env_int("SKEWEIG_BT1_MERGE", 8);
   ctx->c.prm.reorth_w = env_int("SKEWEIG_REORTH_W", 32);
-  if (ctx->c.prm.b < 2 || ctx->c.prm.b > 64 || (ctx->c.prm.b & 1)) ctx->c.prm.b = 64;
   if (ctx->c.prm.bt2_k != 32) ctx->c.prm.bt2_k = 32;
   if (ctx->c.prm.bt1_merge < 1 || ctx->c.prm.bt1_merge > 8) ctx->c.prm.bt1_merge = 8;
   if (ctx->c.prm.reorth_w < 0 || ctx->c.prm.reorth_w > 256) ctx->c.prm.reorth_w = 32;
@@ -271,11 +275,24 @@ const char* skew_status_string(int status) {
   }
 }
 
+// 1 if the lower triangle (strictly lower unless diag) of the device array A holds a NaN or
+// Inf, 0 if not, SKEW_ERR_CUDA on a CUDA failure.  One device pass + one host sync.
+static int check_finite(skew_ctx ctx, Plan& p, const double* A_d, int64_t lda, int64_t n, bool diag) {
+  int* flag = reinterpret_cast<int*>(p.status + 2);
+  int h = 0;
+  CK(nonfinite_lower(A_d, lda, n, diag, flag, ctx->c.stream), "finite check");
+  CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.stream), "finite flag");
+  CK(cudaStreamSynchronize(ctx->c.stream), "sync");
+  return h ? 1 : 0;
+}
+
 // ------------------------------------------------------------------------------------
 // The solve driver shared by skew_eig / skew_eigvals / skew_eig_bse.
 // A_d: device skew input (strictly lower), destroyed.  lam_out/Zre/Zim: device or host.
+// write_z = false: the eigenvectors stay in p.X ([Re | Im], ld p.ldn) for a caller-side epilogue.
 static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t nev, double* lambda, bool lam_host,
-                      double* Zre, double* Zim, int64_t ldz, bool z_host, int64_t k0, int64_t k1) {
+                      double* Zre, double* Zim, int64_t ldz, bool z_host, int64_t k0, int64_t k1,
+                      bool write_z = true) {
   const int64_t nloc = k1 - k0;   // eigenvectors [k0, k1) are computed and returned
   Ctx& c = ctx->c;
   cudaStream_t st = c.stream;
@@ -348,7 +365,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   tstart(ctx, ST_OUT);
   CK(cudaMemcpyAsync(lambda, p.lam, sizeof(double) * nev, lam_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
                      st), "lambda out");
-  if (vec) {
+  if (vec && write_z) {
     if (z_host) {
       CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost, st), "Zre out");
       CK(cudaMemcpy2DAsync(Zim, ldz * 8, p.X + (size_t)p.ldn * nloc, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost,
@@ -401,6 +418,10 @@ static int eig_entry(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t ne
     CK(cudaMemcpy2DAsync(p.Astage, ldad * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, ctx->c.stream), "A in");
     A_d = p.Astage;
   }
+  {   // non-finite input -> argument error
+    const int rc = check_finite(ctx, p, A_d, ldad, n, false);
+    if (rc) return rc == 1 ? -3 : rc;
+  }
   return solve_core(ctx, p, A_d, ldad, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev, k0, k1);
 }
 
@@ -418,39 +439,44 @@ int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, d
   return eig_entry(ctx, n, A, lda, nev, lambda, nullptr, nullptr, n, false, 0, nev, 0);
 }
 
-int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, double* lambda, double* Zre,
+int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, int flags, double* lambda, double* Zre,
                  double* Zim, int64_t ldz, int64_t* pivot_out) {
   if (!ctx) return -1;
   if (n < 2 || (n & 1)) return -2;
   if (!M) return -3;
   if (ldm < n) return -4;
   if (nev < 1 || nev > n / 2) return -5;
-  if (!lambda) return -6;
+  if (flags & ~SKEW_BSE_HAMILTONIAN_Y) return -6;
+  if (!lambda) return -7;
+  if (!Zre && Zim) return -8;
   const bool vec = (Zre != nullptr);
-  if (vec && !Zim) return -8;
-  if (vec && ldz < n) return -9;
+  if (vec && !Zim) return -9;
+  if ((flags & SKEW_BSE_HAMILTONIAN_Y) && !vec) return -8;
+  if (vec && ldz < n) return -10;
   if (pivot_out) *pivot_out = 0;
   CK(cudaSetDevice(ctx->c.device), "set device");
   treset(ctx);
   const bool m_dev = is_device_ptr(M);
   const bool l_dev = is_device_ptr(lambda);
   const bool z_dev = vec ? is_device_ptr(Zre) : m_dev;
-  int flags = (vec ? SKEW_WS_VECTORS : 0) | SKEW_WS_BSE;
+  if (vec && is_device_ptr(Zim) != z_dev) return -9;
+  const int wflags = (vec ? SKEW_WS_VECTORS : 0) | SKEW_WS_BSE | (m_dev ? 0 : SKEW_WS_HOST_STAGING);
   Plan p;
-  if (!ctx->c.ws || !plan_bind(ctx->c, p, n, nev, flags)) {
+  if (!ctx->c.ws || !plan_bind(ctx->c, p, n, nev, wflags)) {
     ctx->c.last_error = "workspace missing or too small";
     return SKEW_ERR_WORKSPACE;
   }
   cudaStream_t st = ctx->c.stream;
   double* M_d = M;
   int64_t ldmd = ldm;
-  if (!m_dev) {
-    // host M: stage it in the (n x n) buffer of the BSE-sized workspace used for L (the
-    // skew W then goes to the X region ... keep it simple: L in Q+X region is not
-    // guaranteed large enough, so host M is staged into Astage and W built in place of
-    // a second buffer is not available) -> require device M for now.
-    ctx->c.last_error = "skew_eig_bse: M must be a device pointer";
-    return -3;
+  if (!m_dev) {   // host M: staged into the workspace (receives L); the host array is not modified
+    ldmd = p.ldn;
+    CK(cudaMemcpy2DAsync(p.Mstage, ldmd * 8, M, ldm * 8, n * 8, n, cudaMemcpyHostToDevice, st), "M in");
+    M_d = p.Mstage;
+  }
+  {
+    const int rc = check_finite(ctx, p, M_d, ldmd, n, true);
+    if (rc) return rc == 1 ? -3 : rc;
   }
   tstart(ctx, ST_BSE);
   const int64_t m = n / 2;
@@ -463,11 +489,28 @@ int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, d
     if (pivot_out) *pivot_out = piv;
     return SKEW_ERR_NOT_DEFINITE;
   }
+  const bool hy = (flags & SKEW_BSE_HAMILTONIAN_Y) != 0;
   int rc = solve_core(ctx, p, p.Astage, p.ldn, nev, lambda, !l_dev, vec ? Zre : nullptr, Zim, ldz, vec && !z_dev, 0,
-                      nev);
+                      nev, !hy);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev_start[ST_BSE], ctx->ev_stop[ST_BSE]);
   ctx->c.stage_ms[ST_BSE] = ms;
+  if (hy && (rc == SKEW_OK || rc == SKEW_ERR_NOCONV)) {
+    // y = J L z (H y = -i lambda y for H = -J M), unnormalised.  W (in
+    // Astage) is consumed by the solve, so Astage takes L [Zre | Zim] (n x 2nev <= n x n).
+    double* Wre = p.Astage;
+    double* Wim = p.Astage + (size_t)p.ldn * nev;
+    CK(bse_lz(M_d, ldmd, n, p.X, p.X + (size_t)p.ldn * nev, p.ldn, nev, Wre, Wim, p.ldn, st), "bse L z");
+    if (z_dev) {
+      CK(bse_apply_J(Wre, Wim, p.ldn, n, nev, Zre, Zim, ldz, st), "bse J y");
+    } else {
+      CK(bse_apply_J(Wre, Wim, p.ldn, n, nev, p.X, p.X + (size_t)p.ldn * nev, p.ldn, st), "bse J y");
+      CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nev, cudaMemcpyDeviceToHost, st), "Yre out");
+      CK(cudaMemcpy2DAsync(Zim, ldz * 8, p.X + (size_t)p.ldn * nev, p.ldn * 8, n * 8, nev, cudaMemcpyDeviceToHost, st),
+         "Yim out");
+    }
+    CK(cudaStreamSynchronize(st), "sync");
+  }
   return rc;
 }
 
@@ -502,11 +545,17 @@ int skew_bse_backtransform(skew_ctx ctx, int64_t n2, const double* L, int64_t ld
   if (ldx < n2) return -10;
   CK(cudaSetDevice(ctx->c.device), "set device");
   cudaStream_t st = ctx->c.stream;
-  double* Y = nullptr;   // Y = L Z (real and imaginary parts), stream-ordered scratch
-  CK(cudaMallocAsync((void**)&Y, sizeof(double) * (size_t)n2 * nev * 2, st), "bse Y alloc");
-  cudaError_t e = bse_backtransform(L, ldl, n2, Zre, Zim, ldz, nev, Y, Y + (size_t)n2 * nev, n2, X, ldx, st);
-  cudaFreeAsync(Y, st);
-  CK(e, "bse backtransform");
+  Arena ar;   // Y = L Z (real and imaginary planes) and the column norms, from the workspace
+  ar.base = (char*)ctx->c.ws;
+  ar.size = ctx->c.ws_bytes;
+  double* Y = ar.take<double>((size_t)n2 * 2 * nev);
+  double* nrm2 = ar.take<double>((size_t)nev);
+  if (!ctx->c.ws || ar.fail || !Y || !nrm2) {
+    ctx->c.last_error = "workspace missing or too small (size it with SKEW_WS_BSE_BACKTRANSFORM)";
+    return SKEW_ERR_WORKSPACE;
+  }
+  CK(bse_backtransform(L, ldl, n2, Zre, Zim, ldz, nev, Y, Y + (size_t)n2 * nev, n2, nrm2, X, ldx, st),
+     "bse backtransform");
   return SKEW_OK;
 }
 

@@ -344,12 +344,16 @@ __global__ void band_copy_kernel(const double* ABin, int64_t ldin, int64_t n, in
 // the dense staircase V (window rows rho = 0..RW-1 start at row s0 + t*b, reflector c at rows
 // rho = c+1 .. c+b), its forward compact-WY T (Q_g = I - V T V^T, dlarft from the Gram
 // matrix) and U = V T^T.  Stored per group as one contiguous block in exactly the shared-
-// memory layout of the apply kernel: [U (K2 x LDW) | V (K2 x LDW)], U[c][rho], V[c][rho],
-// LDW = RW + 4, so that Q_g X = X - V (U^T X) and one bulk copy moves the whole group.
+// memory layout of the apply kernel: [U (K2 x LDU) | -V (K2 x LDV)], U[c][rho], V[c][rho],
+// so that Q_g X = X + (-V) (U^T X) and one bulk copy moves the whole group.  The two row
+// strides differ (LDU = 4, LDV = 6 mod 16 doubles) because the apply kernel reads U with the
+// fragment pattern U[k0+t][c0+g] and V with V[r0+g][c0+2t+s]: both are then bank-conflict free.
 template <int K2, int RW>
 struct BT2Grp {
-  static constexpr int LDW = RW + 4;
-  static constexpr int ELEMS = 2 * K2 * LDW;
+  static constexpr int LDU = RW + 4;
+  static constexpr int LDV = RW + 6;
+  static constexpr int ELEMS = K2 * (LDU + LDV);
+  static_assert(LDU % 16 == 4 && LDV % 16 == 6 && (ELEMS % 2) == 0, "BT2 group layout");
 };
 
 template <int K2, int RW>
@@ -388,15 +392,16 @@ __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const d
     }
     __syncthreads();
     double* out = UV + g * Gp::ELEMS;
-    for (int e = threadIdx.x; e < K2 * Gp::LDW; e += blockDim.x) {
-      int c = e / Gp::LDW, rho = e % Gp::LDW;
-      double u = 0.0, vv = 0.0;
-      if (rho < RW) {
+    for (int e = threadIdx.x; e < K2 * Gp::LDU; e += blockDim.x) {
+      int c = e / Gp::LDU, rho = e % Gp::LDU;
+      double u = 0.0;
+      if (rho < RW)
         for (int c2 = c; c2 < K2; c2++) u += V[c2][rho] * T[c][c2];
-        vv = V[c][rho];
-      }
       out[e] = u;
-      out[K2 * Gp::LDW + e] = vv;
+    }
+    for (int e = threadIdx.x; e < K2 * Gp::LDV; e += blockDim.x) {
+      int c = e / Gp::LDV, rho = e % Gp::LDV;
+      out[K2 * Gp::LDU + e] = (rho < RW) ? -V[c][rho] : 0.0;
     }
     __syncthreads();
   }
@@ -406,158 +411,160 @@ __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const d
 // order sweep blocks last -> first, t ascending.  The RW-row window
 // X[W0 : W0+RW, strip] (W0 = s0 + t*b) lives in a RING-row shared-memory ring: step t+1
 // reuses the last RW-b rows of window t, so per step only b new rows are loaded and b
-// rows are written back.  The next group's [U | V] block (51 KB) arrives with ONE bulk
-// copy (cp.async.bulk, TMA engine) into the second buffer, tracked by an mbarrier; the b
-// new window rows arrive with cp.async (each thread: rows 2*lane.., fixed columns).
-// Per step:  Z = U^T Xw (K2 x NB, DMMA, skip U's zero upper triangle)
-//            Xw -= V Z  (RW x NB, DMMA, skip the staircase's zero fragments)
+// rows are written back.  The next group's [U | -V] block arrives with ONE bulk copy
+// (cp.async.bulk, TMA engine) into the second buffer, tracked by an mbarrier; the b new
+// window rows arrive with cp.async (each thread: rows 2*lane.., fixed columns).
+// Consumers: one warp per 8 columns, so a warp's step needs no other warp's data:
+//            Z^T = Xw^T U         (8 x K2, K = RW; DMMA, U's zero upper triangle skipped)
+//            Xw  = Xw + (-V) Z    (RW x 8, K = K2; Z never leaves the registers: the
+//                                  accumulator fragment of Z^T IS the B fragment of Z when
+//                                  the K2 index is permuted, c = 8i + 2t + s)
 template <int NB, int K2, int RW, int RING, int BB>
 struct BT2Cfg {
   using Gp = BT2Grp<K2, RW>;
+  static constexpr int NCW = NB / 8;     // consumer warps (8 columns each)
+  static constexpr int NPW = 4;          // producer warps
+  static constexpr int THREADS = 32 * (NCW + NPW);
   static constexpr int LDX = RING + 4;   // Xs[col][slot]
-  static constexpr int LDW = Gp::LDW;    // U / V rows
-  static constexpr int LDZ = K2 + 4;     // Zs[col][c]
-  static constexpr int XS = NB * LDX, GS = Gp::ELEMS, ZS = NB * LDZ;
-  static constexpr size_t SMEM = (size_t)(XS + 2 * GS + ZS) * sizeof(double) + 2 * sizeof(uint64_t);
-  static_assert(LDX % 16 == 4 && LDW % 16 == 4 && LDZ % 16 == 4, "pad");
-  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && (NB == 64 || NB == 32), "ring");
+  static constexpr int LDU = Gp::LDU, LDV = Gp::LDV;
+  static constexpr int XS = NB * LDX, GS = Gp::ELEMS;
+  static constexpr size_t SMEM = (size_t)(XS + 2 * GS) * sizeof(double) + 6 * sizeof(uint64_t);
+  static_assert(LDX % 16 == 4, "pad");
+  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && K2 == 32 && (NB == 64 || NB == 32),
+                "ring");
 };
 
-// ring slot of (column, slot) with the bank swizzle of the window ring
-template <int NB, int K2, int RW, int RING, int BB>
-__device__ __forceinline__ int bt2_xo(int col, int slot) {
-  return col * BT2Cfg<NB, K2, RW, RING, BB>::LDX + (slot ^ (((col >> 2) & 1) << 2));
+// Non-volatile DMMA (the compiler may schedule it freely: it has no side effects)
+__device__ __forceinline__ void dmma884f(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-// Z = U^T Xw (K2 x NB): warp (h, column quarter); U[rho][c] = 0 for rho <= c skipped at
-// compile time (H = h); even / odd k-step accumulator sets; next fragments loaded first.
-template <int NB, int K2, int RW, int RING, int H>
-__device__ __forceinline__ void bt2_gemm1(const double* Xs, const double* Us, double* Zs, int off, int warp, int gq,
-                                          int tq) {
-  using C = BT2Cfg<NB, K2, RW, RING, 64>;
-  constexpr int FN = NB / 32;          // column fragments per warp
-  constexpr int NIT = RW / 8;
-  const int n0 = (warp >> 1) * (NB / 4);
-  double acc[2][2][FN][2];
+// Z^T (8 columns x K2) = Xw^T U for the warp's columns cx..cx+7.  A = Xw^T: lane (g, t)
+// reads X[k0+t][cx+g] (ring slot swizzle: slot ^ 4 for columns 4..7 of each group of 8);
+// B = U[k0+t][8i+g].  U[rho][c] = 0 for rho <= c: n-fragment i starts at k-step 2i.
+// Two accumulator sets (even / odd k-steps); fragments of k-step ks+1 loaded before the
+// DMMAs of ks.  Out: z[i][s] = Z[8i + 2t + s][cx + g].
+template <int K2, int RW, int RING, int LDX, int LDU>
+__device__ __forceinline__ void bt2_cw_gemm1(const double* __restrict__ Xs, const double* __restrict__ Us, int off,
+                                             int cx, int gq, int tq, double (&z)[4][2], uint64_t* rows_bar,
+                                             unsigned parity) {
+  constexpr int NKS = RW / 4;
+  constexpr int NRES = (RW - 64) / 4;     // k-steps on the resident rows (rows 0 .. RW-BB-1)
+  static_assert(NRES == 8, "k-step order below assumes RW - BB = 32");
+  // resident k-steps first, paired high / low so every pair has >= 5 live DMMAs (U's zero
+  // triangle leaves k-step ks only 1 + ks/2 live n-fragments for ks < 8); accumulator set =
+  // position parity, so a chain's consecutive DMMAs are >= 4 DMMAs apart
+  constexpr int ORD[8] = {7, 0, 6, 1, 5, 2, 4, 3};
+  double acc[2][4][2];
 #pragma unroll
   for (int p = 0; p < 2; p++)
 #pragma unroll
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < 4; i++) acc[p][i][0] = acc[p][i][1] = 0.0;
+  const double* xcol = Xs + (cx + gq) * LDX;
+  const int swz = gq & 4;
+  const double* ucol = Us + gq * LDU + tq;
+  double a[2], b[2][4];
+  auto ld = [&](int ks, int sb) {
+    int s = off + 4 * ks;
+    if (s >= RING) s -= RING;
+    a[sb] = xcol[(s + tq) ^ swz];
 #pragma unroll
-      for (int j = 0; j < FN; j++) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
-  double fa[2][2][2], fb[2][FN][2];
-  auto ld1 = [&](int it, int sb) {
-    const int kk = it * 8;
-    int slot = off + kk;
-    if (slot >= RING) slot -= RING;
-#pragma unroll
-    for (int j = 0; j < FN; j++) {
-      fb[sb][j][0] = Xs[bt2_xo<NB, K2, RW, RING, 64>(n0 + 8 * j + gq, slot + tq)];
-      fb[sb][j][1] = Xs[bt2_xo<NB, K2, RW, RING, 64>(n0 + 8 * j + gq, slot + 4 + tq)];
-    }
-#pragma unroll
-    for (int i = 0; i < 2; i++) {
-      if (it * 8 + 7 < 8 * (H + 2 * i)) continue;   // fragment entirely zero: not needed
-      const int c = 8 * (H + 2 * i) + gq;
-      fa[sb][i][0] = Us[c * C::LDW + kk + tq];
-      fa[sb][i][1] = Us[c * C::LDW + kk + 4 + tq];
-    }
+    for (int i = 0; i < 4; i++)
+      if (ks >= 2 * i) b[sb][i] = ucol[8 * i * LDU + 4 * ks];
   };
-  ld1(0, 0);
+  ld(ORD[0], 0);
 #pragma unroll
-  for (int it = 0; it < NIT; it++) {
-    const int sb = it & 1;
-    if (it + 1 < NIT) ld1(it + 1, sb ^ 1);
+  for (int p = 0; p < NRES; p++) {
+    const int ks = ORD[p], sb = p & 1;
+    if (p + 1 < NRES) ld(ORD[p + 1], sb ^ 1);
 #pragma unroll
-    for (int i = 0; i < 2; i++) {
-      if (it * 8 + 7 < 8 * (H + 2 * i)) continue;   // U[rho][c] = 0 for rho <= c
+    for (int i = 0; i < 4; i++)
+      if (ks >= 2 * i) dmma884f(acc[p & 1][i][0], acc[p & 1][i][1], a[sb], b[sb][i]);
+  }
+  mbar_wait(rows_bar, parity);   // the producer's new rows (no-op wait if already complete)
+  ld(NRES, 0);
 #pragma unroll
-      for (int j = 0; j < FN; j++) {
-        dmma884(acc[0][i][j][0], acc[0][i][j][1], fa[sb][i][0], fb[sb][j][0]);
-        dmma884(acc[1][i][j][0], acc[1][i][j][1], fa[sb][i][1], fb[sb][j][1]);
-      }
-    }
+  for (int ks = NRES; ks < NKS; ks++) {
+    const int sb = ks & 1;
+    if (ks + 1 < NKS) ld(ks + 1, sb ^ 1);
+#pragma unroll
+    for (int i = 0; i < 4; i++) dmma884f(acc[ks & 1][i][0], acc[ks & 1][i][1], a[sb], b[sb][i]);
   }
 #pragma unroll
-  for (int i = 0; i < 2; i++)
-#pragma unroll
-    for (int j = 0; j < FN; j++) {
-      const int c = 8 * (H + 2 * i) + gq, nn = n0 + 8 * j + 2 * tq;
-      Zs[nn * C::LDZ + c] = acc[0][i][j][0] + acc[1][i][j][0];
-      Zs[(nn + 1) * C::LDZ + c] = acc[0][i][j][1] + acc[1][i][j][1];
-    }
-}
-
-// Xw -= V Z (RW x NB, K = K2): warp (wm = WM, column half); V[rho][c] != 0 iff
-// 1 <= rho - c <= BB, zero fragments skipped at compile time.
-template <int NB, int K2, int RW, int RING, int BB, int WM>
-__device__ __forceinline__ void bt2_gemm2(double* Xs, const double* Vs, const double* Zs, int off, int warp, int gq,
-                                          int tq) {
-  using C = BT2Cfg<NB, K2, RW, RING, BB>;
-  constexpr int FM = RW / 32, FN = NB / 16;
-  constexpr int NIT = K2 / 4;
-  const int n0 = (warp >> 2) * (NB / 2);
-  double acc[FM][FN][2];
-#pragma unroll
-  for (int i = 0; i < FM; i++)
-#pragma unroll
-    for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-  double fa[2][FM], fb[2][FN];
-  auto live = [](int i, int kk) { const int m0 = 8 * (WM + 4 * i); return !(m0 + 7 - kk < 1 || m0 - (kk + 3) > BB); };
-  auto ld2 = [&](int it, int sb) {
-    const int kk = it * 4;
-#pragma unroll
-    for (int j = 0; j < FN; j++) fb[sb][j] = Zs[(n0 + 8 * j + gq) * C::LDZ + kk + tq];
-#pragma unroll
-    for (int i = 0; i < FM; i++)
-      if (live(i, kk)) fa[sb][i] = Vs[(kk + tq) * C::LDW + 8 * (WM + 4 * i) + gq];
-  };
-  ld2(0, 0);
-#pragma unroll
-  for (int it = 0; it < NIT; it++) {
-    const int sb = it & 1, kk = it * 4;
-    if (it + 1 < NIT) ld2(it + 1, sb ^ 1);
-#pragma unroll
-    for (int i = 0; i < FM; i++) {
-      if (!live(i, kk)) continue;
-#pragma unroll
-      for (int j = 0; j < FN; j++) dmma884(acc[i][j][0], acc[i][j][1], fa[sb][i], fb[sb][j]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < FM; i++) {
-    const int m0 = 8 * (WM + 4 * i);
-    int slot = off + m0;
-    if (slot >= RING) slot -= RING;
-#pragma unroll
-    for (int j = 0; j < FN; j++) {
-      const int nn = n0 + 8 * j + 2 * tq;
-      Xs[bt2_xo<NB, K2, RW, RING, BB>(nn, slot + gq)] -= acc[i][j][0];
-      Xs[bt2_xo<NB, K2, RW, RING, BB>(nn + 1, slot + gq)] -= acc[i][j][1];
-    }
+  for (int i = 0; i < 4; i++) {
+    z[i][0] = acc[0][i][0] + acc[1][i][0];
+    z[i][1] = acc[0][i][1] + acc[1][i][1];
   }
 }
 
-// Warp-specialised: 8 consumer warps run only the two DMMA tiles per step; 4 producer warps
-// move the data one step ahead -- it waits until the consumers
+// Xw += (-V) Z for the warp's columns: C fragment = X[8m+g][cx+2t+{0,1}] (loaded from and
+// stored to the ring), A = -V[8m+g][c] and B = z[i][s] with c = 8i + 2t + s (k-step (i, s)).
+// V[rho][c] != 0 only for c+1 <= rho <= c+BB: k-step (i, s) touches m-fragments i .. i+8.
+template <int K2, int RW, int RING, int LDX, int LDV>
+__device__ __forceinline__ void bt2_cw_gemm2(double* __restrict__ Xs, const double* __restrict__ Vs, int off, int cx,
+                                             int gq, int tq, const double (&z)[4][2]) {
+  constexpr int FM = RW / 8;
+  constexpr int SPAN = 9;                 // live m-fragments per k-step
+  double* x0 = Xs + (cx + 2 * tq) * LDX;
+  double* x1 = x0 + LDX;
+  const int swz = (tq & 2) << 1;
+  int slot[FM];
+  double x[FM][2];
+#pragma unroll
+  for (int m = 0; m < FM; m++) {
+    int s = off + 8 * m;
+    if (s >= RING) s -= RING;
+    slot[m] = (s + gq) ^ swz;
+    x[m][0] = x0[slot[m]];
+    x[m][1] = x1[slot[m]];
+  }
+  const double* vb = Vs + 2 * tq * LDV + gq;
+  double va[2][SPAN];
+  auto ld = [&](int kk, int sb) {          // k-step kk = 2i + s
+    const int i = kk >> 1, s = kk & 1;
+    const double* vr = vb + (8 * i + s) * LDV;
+#pragma unroll
+    for (int d = 0; d < SPAN; d++)
+      if (i + d < FM) va[sb][d] = vr[8 * (i + d)];
+  };
+  ld(0, 0);
+#pragma unroll
+  for (int kk = 0; kk < 8; kk++) {
+    const int sb = kk & 1, i = kk >> 1, s = kk & 1;
+    if (kk + 1 < 8) ld(kk + 1, sb ^ 1);
+#pragma unroll
+    for (int d = 0; d < SPAN; d++)
+      if (i + d < FM) dmma884f(x[i + d][0], x[i + d][1], va[sb][d], z[i][s]);
+  }
+#pragma unroll
+  for (int m = 0; m < FM; m++) {
+    x0[slot[m]] = x[m][0];
+    x1[slot[m]] = x[m][1];
+  }
+}
+
+
+// Warp-specialised: NB/8 consumer warps run only the DMMA tiles of their own 8 columns; 4
+// producer warps move the data one step ahead -- it waits until the consumers
 // released step q-1 (mbarrier "empty"), writes that step's leaving rows back to X, then
 // loads step q+1's [U | V] block (one bulk TMA copy) and its new window rows (cp.async)
 // and signals mbarrier "full" (transaction bytes + cp.async completion arrivals).  The
 // ring offset advances by b per step inside a sweep block and by RW at a block boundary,
 // so the next block's first window never overlaps the window being computed.
 template <int NB, int K2, int RW, int RING, int BB, bool SPLIT>
-__global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols, int64_t n,
+__global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_ws_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols, int64_t n,
                                                        const double* __restrict__ UV, const int64_t* __restrict__ gofs,
                                                        int64_t nblk, long long* dbg, int nsplit_arg,
-                                                       unsigned long long* prog) {
+                                                       unsigned long long* prog, int gskew) {
   using C = BT2Cfg<NB, K2, RW, RING, BB>;
   const int nsplit = SPLIT ? nsplit_arg : 1;   // compile-time 1 on the default path
   extern __shared__ __align__(128) double sh[];
   double* Xs = sh;
-  double* G0 = Xs + C::XS;            // [2][U | V]
-  double* Zs = G0 + 2 * C::GS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(Zs + C::ZS);
-  uint64_t* empty = full + 2;
+  double* G0 = Xs + C::XS;            // [2][U | -V]
+  uint64_t* full = reinterpret_cast<uint64_t*>(G0 + 2 * C::GS);   // [U | -V] block landed (bulk tx)
+  uint64_t* empty = full + 2;                                        // consumers released a step
+  uint64_t* fullx = full + 4;                                        // new window rows landed (cp.async)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, tq = lane & 3;
   // nsplit CTAs per strip (wavefront): member m takes the sweep blocks nblk-1-m, nblk-1-m-nsplit, ..
   // Block b only reads rows that block b+1 (the previous member) has written back: a per
@@ -571,18 +578,19 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
   if (nblk <= 0 || blk0 < 0) return;
   for (int e = tid; e < C::XS; e += blockDim.x) Xs[e] = 0.0;   // ring rows beyond n stay finite
   if (tid == 0) {
-    mbar_init(&full[0], 128); mbar_init(&full[1], 128);
-    mbar_init(&empty[0], 8); mbar_init(&empty[1], 8);
+    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+    mbar_init(&fullx[0], 128); mbar_init(&fullx[1], 128);
+    mbar_init(&empty[0], C::NCW); mbar_init(&empty[1], C::NCW);
     mbar_fence_init();
   }
   __syncthreads();
   auto xo = [&](int col, int slot) -> int { return col * C::LDX + (slot ^ (((col >> 2) & 1) << 2)); };
   auto ntask_of = [&](int64_t blk) -> int64_t { return 1 + (n - 3 - blk * K2) / BB; };
 
-  if (warp >= 8) {
+  if (warp >= C::NCW) {
     // ============================ producer (4 warps) ============================
-    const int pw = warp - 8;                       // producer warp: columns pw, pw+4, ...
-    const int ptid = tid - 256;
+    const int pw = warp - C::NCW;                  // producer warp: columns pw, pw+4, ...
+    const int ptid = tid - 32 * C::NCW;
     auto load_rows = [&](int64_t r0, int cnt, int slot0) {   // rows [r0, r0+cnt) -> ring from slot0
       for (int rr = 2 * lane; rr < cnt; rr += 64) {
         int slot = slot0 + rr;
@@ -625,7 +633,7 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
     };
     auto load_group = [&](int64_t g, int b) {
       if (ptid == 0) {
-        mbar_expect_tx_noarrive(&full[b], (unsigned)(C::GS * sizeof(double)));
+        mbar_expect_tx(&full[b], (unsigned)(C::GS * sizeof(double)));
         fence_proxy_async();
         bulk_g2s(G0 + b * C::GS, UV + g * C::GS, (unsigned)(C::GS * sizeof(double)), &full[b]);
       }
@@ -655,7 +663,7 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
     load_group(gofs[blk], 0);
     wait_rows(blk, blk * K2 + RW);
     load_rows(blk * K2, RW, 0);
-    cp_async_mbar_arrive(&full[0]);
+    cp_async_mbar_arrive(&fullx[0]);
     int64_t pblk = -1, pt = 0;
     int poff = 0;
     bool pstored = true;    // step q-1 already written back
@@ -708,7 +716,7 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
           wait_rows(nblk_, nblk_ * K2 + RW);
           load_rows(nblk_ * K2, RW, noff);
         }
-        cp_async_mbar_arrive(&full[b]);
+        cp_async_mbar_arrive(&fullx[b]);
         if (pub_blk >= 0) { publish(pub_blk, pub_rend); pub_blk = -1; }
       }
       pblk = blk; pt = t; poff = off; pstored = stored;
@@ -717,36 +725,34 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
     return;
   }
   // =============================== consumers ===============================
-  long long ph[6] = {0, 0, 0, 0, 0, 0}, tprev = 0, nsteps = 0;
+  long long ph[4] = {0, 0, 0, 0}, tprev = 0, nsteps = 0;
   const bool prof = (dbg != nullptr) && blockIdx.x == 0 && threadIdx.x == 0;
 #define BT2_TS(k) do { if (prof) { long long _t = clock64(); ph[k] += _t - tprev; tprev = _t; } } while (0)
+  const int cx = 8 * warp;   // this warp's columns cx .. cx+7 of the strip
   int64_t blk = blk0, t = 0;
   int off = 0;
+  if (gskew > 0 && (warp & 1)) {   // experiment: odd warps start gskew cycles late
+    const long long t0 = clock64();
+    while (clock64() - t0 < gskew) { }
+  }
   for (int64_t q = 0;; q++) {
     if (prof) { tprev = clock64(); nsteps++; }
-    mbar_wait(&full[q & 1], (unsigned)((q >> 1) & 1));
+    // The [U | -V] block and the window rows have separate barriers: inside a sweep block the
+    // window's first RW-BB rows are this warp's own output of the previous step, so gemm1
+    // starts on them while the producer's new rows are still landing.
+    const unsigned par = (unsigned)((q >> 1) & 1);
+    if (t == 0) mbar_wait(&fullx[q & 1], par);
+    mbar_wait(&full[q & 1], par);
     BT2_TS(0);
     const double* Us = G0 + (q & 1) * C::GS;
-    const double* Vs = Us + K2 * C::LDW;
-      // ---- Z = U^T Xw : warps 2 (M: c fragments {h, h+2}, interleaved to balance U's zero
-      //      upper triangle) x 4 (N: NB/4 columns).  The zero-fragment pattern depends on h
-      //      only: compile-time per h, so skipped fragments issue nothing.
-      if (warp & 1) bt2_gemm1<NB, K2, RW, RING, 1>(Xs, Us, Zs, off, warp, gq, tq);
-      else bt2_gemm1<NB, K2, RW, RING, 0>(Xs, Us, Zs, off, warp, gq, tq);
-      named_bar(1 + (warp >> 2), 128);   // two independent 4-warp groups (columns 0-31 / 32-63)
-      BT2_TS(2);
-      // ---- Xw -= V Z : warps 4 (M, interleaved row fragments: balanced staircase work) x 2
-      //      (N); the staircase pattern depends on wm only: compile-time per wm.
-      switch (warp & 3) {
-        case 0: bt2_gemm2<NB, K2, RW, RING, BB, 0>(Xs, Vs, Zs, off, warp, gq, tq); break;
-        case 1: bt2_gemm2<NB, K2, RW, RING, BB, 1>(Xs, Vs, Zs, off, warp, gq, tq); break;
-        case 2: bt2_gemm2<NB, K2, RW, RING, BB, 2>(Xs, Vs, Zs, off, warp, gq, tq); break;
-        default: bt2_gemm2<NB, K2, RW, RING, BB, 3>(Xs, Vs, Zs, off, warp, gq, tq); break;
-      }
+    const double* Vs = Us + K2 * C::LDU;
+    double z[4][2];
+    bt2_cw_gemm1<K2, RW, RING, C::LDX, C::LDU>(Xs, Us, off, cx, gq, tq, z, &fullx[q & 1], par);
+    BT2_TS(1);
+    bt2_cw_gemm2<K2, RW, RING, C::LDX, C::LDV>(Xs, Vs, off, cx, gq, tq, z);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[q & 1]);
-    named_bar(1 + (warp >> 2), 128);   // two independent 4-warp groups (columns 0-31 / 32-63)
-    BT2_TS(3);
+    BT2_TS(2);
     // advance
     int64_t nt = t + 1;
     int noff = off + BB;
@@ -756,7 +762,8 @@ __global__ void __launch_bounds__(384, 1) bt2_ws_kernel(double* __restrict__ X, 
     t = nt; off = noff;
   }
   if (prof) {
-    for (int k = 0; k < 5; k++) dbg[k] = ph[k];
+    for (int k = 0; k < 3; k++) dbg[k] = ph[k];
+    dbg[3] = 0; dbg[4] = 0;
     dbg[5] = nsteps;
   }
 #undef BT2_TS
@@ -796,7 +803,7 @@ void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w) {
   int64_t ng = std::max<int64_t>(L.ngroups, 1);
   w.qv = ar.take<double>((size_t)ng * L.k2 * L.b);
   w.qtau = ar.take<double>((size_t)ng * L.k2);
-  if (vectors) w.qT = ar.take<double>((size_t)ng * 2 * L.k2 * (L.b + L.k2 + 4));   // [U | V] per group
+  if (vectors) w.qT = ar.take<double>((size_t)ng * L.k2 * (2 * (L.b + L.k2) + 10));   // [U | -V] per group (BT2Grp)
   w.gofs = ar.take<int64_t>(std::max<int64_t>(L.nblk, 1));
   if (vectors) w.prog = ar.take<unsigned long long>((size_t)4 * 2 * ((L.n + 63) / 64 + 1));   // BT2 wavefront flags
 }
@@ -911,6 +918,8 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
   if (const char* v = getenv("SKEWEIG_BT2_NB")) n64 = (atoi(v) == 32) ? 0 : s64;   // experiments
   if (n64 != s64) nsplit = 1;
   const int64_t c64 = std::min<int64_t>(ncols, 64 * n64), c32 = ncols - c64;
+  int gskew = 0;
+  if (const char* v = getenv("SKEWEIG_BT2_SKEW")) gskew = atoi(v);   // experiments
   auto launch = [&](auto kern, size_t smem, int NBv, int64_t cbeg, int64_t cnt, int ns) -> cudaError_t {
     if (cnt <= 0) return cudaSuccess;
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -921,7 +930,8 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
       if (e2) return e2;
     }
     KScope ks(KC_BT2, st);
-    kern<<<(unsigned)grid, 384, smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp, ns, w.prog);
+    kern<<<(unsigned)grid, 32 * (NBv / 8 + 4), smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp, ns, w.prog,
+                                            gskew);
     return cudaGetLastError();
   };
   if (nsplit > 1)
@@ -938,8 +948,8 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
     long long h[6];
     cudaMemcpyAsync(h, dbgp, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    fprintf(stderr, "[bt2 dbg] steps %lld  per-step cycles: wait %.0f prefetch %.0f gemm1 %.0f gemm2 %.0f store %.0f\n",
-            h[5], (double)h[0] / h[5], (double)h[1] / h[5], (double)h[2] / h[5], (double)h[3] / h[5], (double)h[4] / h[5]);
+    fprintf(stderr, "[bt2 dbg] steps %lld  per-step cycles (warp 0): wait %.0f gemm1 %.0f gemm2 %.0f\n", h[5],
+            (double)h[0] / h[5], (double)h[1] / h[5], (double)h[2] / h[5]);
     cudaFree(dbgp);
   }
   return cudaGetLastError();

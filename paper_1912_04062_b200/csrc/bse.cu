@@ -83,18 +83,19 @@ __global__ void chol_trsm_kernel(double* M, int64_t ldm, int64_t j0, int nb, int
 }
 
 __global__ void zero_upper_kernel(double* M, int64_t ldm, int64_t n) {
-  int64_t j = blockIdx.y;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < j; i += (int64_t)gridDim.x * blockDim.x)
-    M[SK_IDX(i, j, ldm)] = 0.0;
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y)   // grid.y is capped at 65535
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < j; i += (int64_t)gridDim.x * blockDim.x)
+      M[SK_IDX(i, j, ldm)] = 0.0;
 }
 
 // W11 strictly lower = S - S^T ; W22 strictly lower = 0 ; (W21 written by GEMM)
 __global__ void w11_kernel(const double* S, int64_t lds, int64_t m, double* W, int64_t ldw) {
-  int64_t j = blockIdx.y;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-    if (i > j) {
-      W[SK_IDX(i, j, ldw)] = S[SK_IDX(i, j, lds)] - S[SK_IDX(j, i, lds)];
-      W[SK_IDX(m + i, m + j, ldw)] = 0.0;
+  for (int64_t j = blockIdx.y; j < m; j += gridDim.y) {   // grid.y is capped at 65535
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+      if (i > j) {
+        W[SK_IDX(i, j, ldw)] = S[SK_IDX(i, j, lds)] - S[SK_IDX(j, i, lds)];
+        W[SK_IDX(m + i, m + j, ldw)] = 0.0;
+      }
     }
   }
 }
@@ -124,7 +125,7 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
     }
   }
   {
-    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
+    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
     zero_upper_kernel<<<grid, 256, 0, st>>>(M, ldm, n);
   }
   const int64_t m = n / 2;
@@ -146,7 +147,7 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
     if (e) return e;
   }
   {
-    dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 64), (unsigned)std::max<int64_t>(m, 1));
+    dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 64), (unsigned)std::min<int64_t>(std::max<int64_t>(m, 1), 65535));
     w11_kernel<<<grid, 256, 0, st>>>(S, lds, m, W, ldw);
   }
   return cudaGetLastError();
@@ -161,19 +162,20 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
 __global__ void bse_build_M_kernel(const double2* __restrict__ A, int64_t lda, const double2* __restrict__ B,
                                    int64_t ldb, int64_t n, double* __restrict__ M, int64_t ldm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t j = blockIdx.y;
   if (i >= n) return;
-  const double2 a = A[SK_IDX(i, j, lda)], b = B[SK_IDX(i, j, ldb)];
-  M[SK_IDX(i, j, ldm)] = a.x + b.x;            // Re(A+B)
-  M[SK_IDX(i, n + j, ldm)] = a.y - b.y;        // Im(A-B)
-  M[SK_IDX(n + i, j, ldm)] = -(a.y + b.y);     // -Im(A+B)
-  M[SK_IDX(n + i, n + j, ldm)] = a.x - b.x;    // Re(A-B)
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {   // grid.y is capped at 65535
+    const double2 a = A[SK_IDX(i, j, lda)], b = B[SK_IDX(i, j, ldb)];
+    M[SK_IDX(i, j, ldm)] = a.x + b.x;            // Re(A+B)
+    M[SK_IDX(i, n + j, ldm)] = a.y - b.y;        // Im(A-B)
+    M[SK_IDX(n + i, j, ldm)] = -(a.y + b.y);     // -Im(A+B)
+    M[SK_IDX(n + i, n + j, ldm)] = a.x - b.x;    // Re(A-B)
+  }
 }
 
 cudaError_t bse_build_M(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t n, double* M, int64_t ldm,
                         cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  dim3 grid((unsigned)((n + 255) / 256), (unsigned)n);
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)std::min<int64_t>(n, 65535));
   bse_build_M_kernel<<<grid, 256, 0, st>>>((const double2*)A, lda, (const double2*)B, ldb, n, M, ldm);
   return cudaGetLastError();
 }
@@ -227,32 +229,115 @@ __global__ void __launch_bounds__(256) bse_trmm_kernel(const double* __restrict_
     }
 }
 
-// Step 4, part 2: x = Q J y with J = [[0, I], [-I, 0]] and Q = [[I, -iI], [I, iI]] / sqrt(2)
-// (Theorem 1):  x_top = (y2 + i y1) / sqrt 2,  x_bot = (y2 - i y1) / sqrt 2
-// for y = [y1; y2] (n rows each), written interleaved complex.
-__global__ void bse_qj_kernel(const double* __restrict__ Yre, const double* __restrict__ Yim, int64_t ldy, int64_t n,
-                              double2* __restrict__ X, int64_t ldx) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t j = blockIdx.y;
-  if (i >= n) return;
-  const double s = 0.70710678118654752440;
-  const double y1r = Yre[SK_IDX(i, j, ldy)], y1i = Yim[SK_IDX(i, j, ldy)];
-  const double y2r = Yre[SK_IDX(n + i, j, ldy)], y2i = Yim[SK_IDX(n + i, j, ldy)];
-  X[SK_IDX(i, j, ldx)] = make_double2(s * (y2r - y1i), s * (y2i + y1r));
-  X[SK_IDX(n + i, j, ldx)] = make_double2(s * (y2r + y1i), s * (y2i - y1r));
+// Squared 2-norms of the columns of y = [Yre | Yim] (n2 rows): one CTA per column
+// (grid-stride), fixed-order block reduction (deterministic).
+__global__ void __launch_bounds__(256) bse_colnorm2_kernel(const double* __restrict__ Yre,
+                                                           const double* __restrict__ Yim, int64_t ldy, int64_t n2,
+                                                           int64_t nev, double* __restrict__ nrm2) {
+  __shared__ double red[8];
+  for (int64_t j = blockIdx.x; j < nev; j += gridDim.x) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
+      const double a = Yre[SK_IDX(i, j, ldy)], b = Yim[SK_IDX(i, j, ldy)];
+      s = fma(a, a, fma(b, b, s));
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; w++) t += red[w];
+      nrm2[j] = t;
+    }
+    __syncthreads();
+  }
 }
 
-cudaError_t bse_backtransform(const double* L, int64_t ldl, int64_t n2, const double* Zre, const double* Zim,
-                              int64_t ldz, int64_t nev, double* Yre, double* Yim, int64_t ldy, double* X, int64_t ldx,
-                              cudaStream_t st) {
+// Step 4, part 2: x = Q J y / ||y|| with J = [[0, I], [-I, 0]] and Q = [[I, -iI], [I, iI]] /
+// sqrt(2) (Theorem 1):  x_top = (y2 + i y1) / sqrt 2,  x_bot = (y2 - i y1) /
+// sqrt 2 for y = [y1; y2] (n rows each), written interleaved complex.  ||Q J y|| = ||y||
+// (Q, J unitary), so dividing by ||y|| gives unit 2-norm x (reading R22).
+__global__ void bse_qj_kernel(const double* __restrict__ Yre, const double* __restrict__ Yim, int64_t ldy, int64_t n,
+                              int64_t nev, const double* __restrict__ nrm2, double2* __restrict__ X, int64_t ldx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int64_t j = blockIdx.y; j < nev; j += gridDim.y) {   // grid.y is capped at 65535
+    const double nn = nrm2[j];
+    const double s = 0.70710678118654752440 / (nn > 0.0 ? sqrt(nn) : 1.0);
+    const double y1r = Yre[SK_IDX(i, j, ldy)], y1i = Yim[SK_IDX(i, j, ldy)];
+    const double y2r = Yre[SK_IDX(n + i, j, ldy)], y2i = Yim[SK_IDX(n + i, j, ldy)];
+    X[SK_IDX(i, j, ldx)] = make_double2(s * (y2r - y1i), s * (y2i + y1r));
+    X[SK_IDX(n + i, j, ldx)] = make_double2(s * (y2r + y1i), s * (y2i - y1r));
+  }
+}
+
+// y = J w for w = [w1; w2] (n rows each), real and imaginary planes: y1 = w2, y2 = -w1
+// (skew_eig_bse with SKEW_BSE_HAMILTONIAN_Y: w = L z, y = J L z, H y = -i lambda y for
+// H = -J M).
+__global__ void bse_j_kernel(const double* __restrict__ Wre, const double* __restrict__ Wim, int64_t ldw, int64_t n,
+                             int64_t nev, double* __restrict__ Yre, double* __restrict__ Yim, int64_t ldy) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int64_t j = blockIdx.y; j < nev; j += gridDim.y) {
+    const double a = Wre[SK_IDX(i, j, ldw)], b = Wim[SK_IDX(i, j, ldw)];
+    const double c = Wre[SK_IDX(n + i, j, ldw)], d = Wim[SK_IDX(n + i, j, ldw)];
+    Yre[SK_IDX(i, j, ldy)] = c;
+    Yim[SK_IDX(i, j, ldy)] = d;
+    Yre[SK_IDX(n + i, j, ldy)] = -a;
+    Yim[SK_IDX(n + i, j, ldy)] = -b;
+  }
+}
+
+cudaError_t bse_lz(const double* L, int64_t ldl, int64_t n2, const double* Zre, const double* Zim, int64_t ldz,
+                   int64_t nev, double* Yre, double* Yim, int64_t ldy, cudaStream_t st) {
   if (n2 <= 0 || nev <= 0) return cudaSuccess;
   dim3 g1((unsigned)((n2 + kTM - 1) / kTM), (unsigned)((nev + kTM - 1) / kTM), 2);
   bse_trmm_kernel<<<g1, 256, 0, st>>>(L, ldl, n2, Zre, Zim, ldz, nev, Yre, Yim, ldy);
-  cudaError_t e = cudaGetLastError();
+  return cudaGetLastError();
+}
+
+cudaError_t bse_apply_J(const double* Wre, const double* Wim, int64_t ldw, int64_t n2, int64_t nev, double* Yre,
+                        double* Yim, int64_t ldy, cudaStream_t st) {
+  if (n2 <= 0 || nev <= 0) return cudaSuccess;
+  const int64_t n = n2 / 2;
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)std::min<int64_t>(nev, 65535));
+  bse_j_kernel<<<g, 256, 0, st>>>(Wre, Wim, ldw, n, nev, Yre, Yim, ldy);
+  return cudaGetLastError();
+}
+
+cudaError_t bse_backtransform(const double* L, int64_t ldl, int64_t n2, const double* Zre, const double* Zim,
+                              int64_t ldz, int64_t nev, double* Yre, double* Yim, int64_t ldy, double* nrm2,
+                              double* X, int64_t ldx, cudaStream_t st) {
+  if (n2 <= 0 || nev <= 0) return cudaSuccess;
+  cudaError_t e = bse_lz(L, ldl, n2, Zre, Zim, ldz, nev, Yre, Yim, ldy, st);
+  if (e != cudaSuccess) return e;
+  bse_colnorm2_kernel<<<(unsigned)std::min<int64_t>(nev, 4096), 256, 0, st>>>(Yre, Yim, ldy, n2, nev, nrm2);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t n = n2 / 2;
-  dim3 g2((unsigned)((n + 255) / 256), (unsigned)nev);
-  bse_qj_kernel<<<g2, 256, 0, st>>>(Yre, Yim, ldy, n, (double2*)X, ldx);
+  dim3 g2((unsigned)((n + 255) / 256), (unsigned)std::min<int64_t>(nev, 65535));
+  bse_qj_kernel<<<g2, 256, 0, st>>>(Yre, Yim, ldy, n, nev, nrm2, (double2*)X, ldx);
+  return cudaGetLastError();
+}
+
+// Non-finite scan of a column-major n x n input: entries i > j (skew A, strictly lower) or
+// i >= j (symmetric M, lower with diagonal).  flag: device int, set to 1 on any NaN / Inf.
+__global__ void nonfinite_lower_kernel(const double* __restrict__ A, int64_t lda, int64_t n, int diag,
+                                       int* __restrict__ flag) {
+  int bad = 0;
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    const int64_t i0 = j + (diag ? 0 : 1);
+    for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      bad |= !isfinite(A[SK_IDX(i, j, lda)]);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+cudaError_t nonfinite_lower(const double* A, int64_t lda, int64_t n, bool diag, int* flag_d, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(flag_d, 0, sizeof(int), st);
+  if (e != cudaSuccess || n <= 0) return e;
+  dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 4), (unsigned)std::min<int64_t>(n, 65535));
+  nonfinite_lower_kernel<<<g, 256, 0, st>>>(A, lda, n, diag ? 1 : 0, flag_d);
   return cudaGetLastError();
 }
 

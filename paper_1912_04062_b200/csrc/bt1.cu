@@ -189,17 +189,17 @@ cudaError_t bt1_apply(const F2BLayout& L, const double* vstore, const double* ta
 // Output split: Zre = X[:, :nev], Zim = X[:, nev:] into the caller's ldz layout.
 __global__ void split_output_kernel(const double* X, int64_t ldx, int64_t n, int64_t nev, double* Zre, double* Zim,
                                     int64_t ldz) {
-  int64_t c = blockIdx.y;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    Zre[SK_IDX(i, c, ldz)] = X[SK_IDX(i, c, ldx)];
-    Zim[SK_IDX(i, c, ldz)] = X[SK_IDX(i, nev + c, ldx)];
-  }
+  for (int64_t c = blockIdx.y; c < nev; c += gridDim.y)   // grid.y is capped at 65535
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      Zre[SK_IDX(i, c, ldz)] = X[SK_IDX(i, c, ldx)];
+      Zim[SK_IDX(i, c, ldz)] = X[SK_IDX(i, nev + c, ldx)];
+    }
 }
 
 cudaError_t split_output(const double* X, int64_t ldx, int64_t n, int64_t nev, double* Zre, double* Zim, int64_t ldz,
                          cudaStream_t st) {
   if (nev <= 0) return cudaSuccess;
-  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)nev);
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(nev, 65535));
   KScope ks(KC_OUT, st);
   split_output_kernel<<<grid, 256, 0, st>>>(X, ldx, n, nev, Zre, Zim, ldz);
   return cudaGetLastError();

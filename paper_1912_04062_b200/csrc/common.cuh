@@ -4,10 +4,32 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #define SK_IDX(i, j, ld) ((size_t)(i) + (size_t)(j) * (size_t)(ld))
 
 namespace sk {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
+// belongs to the device's context, so a process-wide "already set" flag would skip it for
+// a context on a second device.  Thread-safe (distinct contexts may run on distinct host
+// threads).
+inline cudaError_t set_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(kern, dev);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
 
 template <class T>
 __host__ __device__ __forceinline__ T smin(T a, T b) { return a < b ? a : b; }

@@ -985,12 +985,8 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   const char* hh = getenv("SKEWEIG_PANEL_HH");   // experiments: force the Householder panel
   if (b == 64 && m >= b && Rc >= b && cqr_smem <= 200 * 1024 && (size_t)b * Rc * sizeof(double) + extra <= 200 * 1024 &&
       !(hh && hh[0] == '1')) {
-    static bool set = false;
-    if (!set) {
-      e = cudaFuncSetAttribute(panel_cqr_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + (int)extra);
-      if (e) return e;
-      set = true;
-    }
+    e = set_smem_attr((const void*)panel_cqr_kernel<64>, 200 * 1024 + (int)extra);
+    if (e) return e;
     CqrArgs ca;
     ca.p = a;
     ca.p.R = Rc;
@@ -1022,15 +1018,11 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
     }
   }
   if (use_smem) {
-    static bool set = false;
-    if (!set) {
-      e = cudaFuncSetAttribute(panel_qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + (int)extra);
-      if (e) return e;
-      set = true;
-    }
+    e = set_smem_attr((const void*)panel_qr_kernel<true>, 200 * 1024 + (int)extra);
+    if (e) return e;
     e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel<true>, dim3(G), dim3(256), args, smem_full, st);
   } else {
-    e = cudaFuncSetAttribute(panel_qr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)extra);
+    e = set_smem_attr((const void*)panel_qr_kernel<false>, (int)extra);
     if (e) return e;
     e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel<false>, dim3(G), dim3(256), args, extra, st);
   }
@@ -1067,13 +1059,8 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     using TR = GemmTile<kSymmBM, 64, kSymmBK, 32, 32, kSymmStages, false, false>;
     using TC = GemmTile<kSymmBM, 64, kSymmBK, 32, 32, kSymmStages, true, false>;
     size_t smem = std::max(TR::SMEM_BYTES, TC::SMEM_BYTES);
-    static bool set = false;
-    if (!set) {
-      e = cudaFuncSetAttribute(symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e) return e;
-      set = true;
-    }
+    e = set_smem_attr((const void*)symm_kernel<kSymmBM, 64, kSymmBK, kSymmStages>, (int)smem);
+    if (e) return e;
     const int64_t nt = (m + kSymmBM - 1) / kSymmBM;
     int64_t grid = nt;
     int split = 1;

@@ -253,11 +253,9 @@ cudaError_t gemm_dmma(const GemmArgs& g, cudaStream_t st) {
   GemmArgs ga = g;
   ga.vec = gemm_vec_ok(g.A, g.lda, g.B, g.ldb) ? 1 : 0;
   auto kern = gemm_dmma_kernel<BM, BN, BK, WM, WN, STAGES, A_KMAJ, B_NMAJ, TRI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_BYTES);
+  {
+    cudaError_t e = set_smem_attr((const void*)kern, (int)T::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   int64_t tm = (g.M + BM - 1) / BM, tn = (g.N + BN - 1) / BN;
   dim3 grid;

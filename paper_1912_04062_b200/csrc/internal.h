@@ -14,11 +14,12 @@ struct Arena {
   char* base = nullptr;
   size_t size = 0, off = 0;
   bool measuring = false;   // size-query mode: only accumulate
+  bool fail = false;        // some take() did not fit
   template <class T>
   T* take(size_t count) {
     size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
     if (measuring) { off += bytes; return nullptr; }
-    if (off + bytes > size) return nullptr;
+    if (off + bytes > size) { fail = true; return nullptr; }
     T* p = reinterpret_cast<T*>(base + off);
     off += bytes;
     return p;
@@ -26,7 +27,7 @@ struct Arena {
 };
 
 struct Params {
-  int b = 64;            // band width (F2B panel width), SKEWEIG_B
+  int b = 64;            // band width (F2B panel width), fixed
   int bt2_k = 32;        // BT2 group width (sweeps per group), SKEWEIG_BT2_K
   int bt1_merge = 8;     // F2B panels merged per BT1 block reflector, SKEWEIG_BT1_MERGE
   int reorth_w = 32;     // inverse-iteration reorthogonalisation window, SKEWEIG_REORTH_W
@@ -233,7 +234,12 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
 cudaError_t bse_build_M(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t n, double* M, int64_t ldm,
                         cudaStream_t st);
 cudaError_t bse_backtransform(const double* L, int64_t ldl, int64_t n2, const double* Zre, const double* Zim,
-                              int64_t ldz, int64_t nev, double* Yre, double* Yim, int64_t ldy, double* X, int64_t ldx,
-                              cudaStream_t st);
+                              int64_t ldz, int64_t nev, double* Yre, double* Yim, int64_t ldy, double* nrm2,
+                              double* X, int64_t ldx, cudaStream_t st);
+cudaError_t bse_lz(const double* L, int64_t ldl, int64_t n2, const double* Zre, const double* Zim, int64_t ldz,
+                   int64_t nev, double* Yre, double* Yim, int64_t ldy, cudaStream_t st);
+cudaError_t bse_apply_J(const double* Wre, const double* Wim, int64_t ldw, int64_t n2, int64_t nev, double* Yre,
+                        double* Yim, int64_t ldy, cudaStream_t st);
+cudaError_t nonfinite_lower(const double* A, int64_t lda, int64_t n, bool diag, int* flag_d, cudaStream_t st);
 
 }  // namespace sk

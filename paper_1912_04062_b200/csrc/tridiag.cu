@@ -430,7 +430,7 @@ __global__ void td_apply_rinv(double* Y, int64_t ldy, int nb, const double* Rinv
 // X[:, c] = Re(D q_c), X[:, nev + c] = Im(D q_c); row k: k%4 = 0 -> Re +q, 1 -> Im +q,
 // 2 -> Re -q, 3 -> Im -q.
 __global__ void assemble_D_kernel(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx) {
-  int64_t c = blockIdx.y;
+  for (int64_t c = blockIdx.y; c < nev; c += gridDim.y)   // grid.y is capped at 65535
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     double q = Q[SK_IDX(k, c, ldq)];
     double re = 0.0, im = 0.0;
@@ -712,11 +712,9 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
 static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* Y, int64_t ldy, int nb, int64_t n,
                                   TridWork& w, cudaStream_t st) {
   int64_t nchunks = (n + kGramRows - 1) / kGramRows;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(td_gram_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+  {
+    cudaError_t e = set_smem_attr((const void*)td_gram_partial, 120 * 1024);
     if (e) return e;
-    attr = true;
   }
   KScope ks(KC_TRID_REORTH, st, 2);
   td_gram_partial<<<(unsigned)nchunks, 256, (size_t)(p + nb) * (kGramRows + 1) * 8, st>>>(Qp, ldq, p, Y, ldy, nb, n,
@@ -884,12 +882,8 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     const char* fz = getenv("SKEWEIG_REORTH_FUSED");   // experiments: 0 = kernel-per-step path
     fused = smem <= 227 * 1024 && !(fz && fz[0] == '0');
     if (fused) {
-      static bool attr = false;
-      if (!attr) {
-        e = cudaFuncSetAttribute(td_reorth_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e) return e;
-        attr = true;
-      }
+      e = set_smem_attr((const void*)td_reorth_fused_kernel, 227 * 1024);
+      if (e) return e;
       int occ = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, td_reorth_fused_kernel, 256, smem);
       fused = occ * nsm >= G;
@@ -971,7 +965,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
 
 cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st) {
   if (nev <= 0) return cudaSuccess;
-  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)nev);
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(nev, 65535));
   KScope ks(KC_ASSEMBLE, st);
   assemble_D_kernel<<<grid, 256, 0, st>>>(Q, ldq, n, nev, X, ldx);
   return cudaGetLastError();

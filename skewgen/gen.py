@@ -50,7 +50,13 @@ def random_skew_lower_colmajor(n, seed, lda=None):
     the diagonal and upper triangle are zero (never read by either side)."""
     lda = n if lda is None else lda
     A = np.zeros((lda, n), dtype=np.float64, order="F")
-    A[:n, :n] = np.tril(random_skew(n, seed), -1)
+    # column blocks written in place (same entries as random_skew's lower triangle,
+    # without materialising the dense n x n matrix and its transpose)
+    for j0 in range(0, n, 256):
+        j1 = min(n, j0 + 256)
+        jj, ii = np.meshgrid(np.arange(j0, j1), np.arange(n), indexing="xy")
+        vals = uniform_pm1(_keys(seed, n, ii, jj))
+        A[:n, j0:j1] = np.where(ii > jj, vals, 0.0)
     return A
 
 

@@ -370,8 +370,92 @@ def test_bse_hbs_pipeline_vs_oracle(sk, n, nev):
     assert np.max(np.linalg.norm(H @ X - X * lam, axis=0) / nx) <= 1e-12 * nH
     cos = np.abs(np.sum(X_o.conj() * X, axis=0)) / (nx * np.linalg.norm(X_o, axis=0))
     assert np.min(cos) >= 1 - 1e-9
-    # the Q J L map preserves the skew solver's normalisation: ||x|| = ||L z||
-    assert np.allclose(nx, np.linalg.norm(X_o, axis=0), rtol=1e-9)
+    # unit 2-norm eigenvectors, like the oracle's
+    assert np.max(np.abs(nx - 1.0)) <= 1e-13
+    assert np.max(np.abs(np.linalg.norm(X_o, axis=0) - 1.0)) <= 1e-13
+
+
+def test_bse_hamiltonian_y(sk):
+    """skew_eig_bse with SKEW_BSE_HAMILTONIAN_Y: y_k = J L z_k satisfies H y = -i lam y for
+    H = -J M, pinned by that residual (its normalisation is open)."""
+    n = 256
+    M = skewgen.bse_spd(n, 4242)
+    lam, Yre, Yim = sk.skew_eig_bse(_cuda(M), hamiltonian_y=True)
+    lam, Y = lam.cpu().numpy(), Yre.cpu().numpy() + 1j * Yim.cpu().numpy()
+    J = skewgen.J_matrix(n)
+    H = -J @ M
+    ny = np.linalg.norm(Y, axis=0)
+    assert np.min(ny) > 0.1
+    res = np.linalg.norm(H @ Y + 1j * Y * lam, axis=0) / ny
+    assert np.max(res) <= 1e-12 * np.linalg.norm(H)
+    lam_o = oracle.bse_eig(M, want_vectors=False)[0]
+    assert np.max(np.abs(lam - lam_o)) <= 1e-12 * np.linalg.norm(H)
+
+
+def test_bse_host_M_matches_device(sk):
+    """skew_eig_bse with HOST M / lambda / Zre / Zim (staged through the workspace) gives the
+    device call's result bit for bit and leaves the host M untouched."""
+    n = 130
+    M = np.asfortranarray(skewgen.bse_spd(n, 77))
+    M0 = M.copy()
+    c = sk.Context()
+    c.ensure_workspace(n, n // 2, sk.SKEW_WS_VECTORS | sk.SKEW_WS_BSE | sk.SKEW_WS_HOST_STAGING)
+    lam = np.zeros(n // 2)
+    Zre = np.zeros((n, n // 2), order="F")
+    Zim = np.zeros((n, n // 2), order="F")
+    piv = __import__("ctypes").c_int64(0)
+    rc = sk.lib().skew_eig_bse(c.h, n, M.ctypes.data, n, n // 2, 0, lam.ctypes.data, Zre.ctypes.data,
+                               Zim.ctypes.data, n, __import__("ctypes").byref(piv))
+    assert rc == 0, c.last_error()
+    assert np.array_equal(M, M0)
+    lam_d, Zre_d, Zim_d = sk.skew_eig_bse(_cuda(M0), ctx=c)
+    assert np.array_equal(lam, lam_d.cpu().numpy())
+    assert np.array_equal(Zre, Zre_d.cpu().numpy()) and np.array_equal(Zim, Zim_d.cpu().numpy())
+
+
+def test_nonfinite_input_rejected(sk):
+    """A NaN / Inf in the triangle that is read is an argument error (-3), SURVEY 8(b)."""
+    n = 100
+    L = sk.lib()
+    c = sk.Context()
+    c.ensure_workspace(n, n // 2, sk.SKEW_WS_VECTORS | sk.SKEW_WS_BSE)
+    lam = torch.empty(n // 2, dtype=torch.float64, device="cuda")
+    Z = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    for bad in (float("nan"), float("inf")):
+        A = torch.from_numpy(skewgen.random_skew_lower_colmajor(n, 5)).cuda().t().contiguous().t()
+        A[n - 1, 3] = bad
+        assert L.skew_eig(c.h, n, A.data_ptr(), n, n // 2, lam.data_ptr(), Z.data_ptr(),
+                          Z.data_ptr() + 8 * n * (n // 2), n) == -3
+        assert L.skew_eigvals(c.h, n, A.data_ptr(), n, n // 2, lam.data_ptr()) == -3
+        M = torch.from_numpy(skewgen.bse_spd(n, 5)).cuda()
+        M[7, 7] = bad
+        assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, n // 2, 0, lam.data_ptr(), None, None, n, None) == -3
+    # the upper triangle is never read: a NaN there is fine
+    A = torch.from_numpy(skewgen.random_skew_lower_colmajor(n, 5)).cuda().t().contiguous().t()
+    A[3, n - 1] = float("nan")
+    assert L.skew_eigvals(c.h, n, A.data_ptr(), n, n // 2, lam.data_ptr()) == 0
+
+
+def test_bse_bad_arguments(sk):
+    n = 8
+    L = sk.lib()
+    c = sk.Context()
+    c.ensure_workspace(n, n // 2, sk.SKEW_WS_VECTORS | sk.SKEW_WS_BSE)
+    M = torch.from_numpy(skewgen.bse_spd(n, 5)).cuda()
+    lam = torch.empty(n, dtype=torch.float64, device="cuda")
+    Z = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    assert L.skew_eig_bse(c.h, 7, M.data_ptr(), n, 2, 0, lam.data_ptr(), None, None, n, None) == -2
+    assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, 2, 2, lam.data_ptr(), None, None, n, None) == -6
+    assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, 2, 0, None, None, None, n, None) == -7
+    assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, 2, 0, lam.data_ptr(), None, Z.data_ptr(), n, None) == -8
+    assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, 2, 0, lam.data_ptr(), Z.data_ptr(), None, n, None) == -9
+    assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, 2, 1, lam.data_ptr(), None, None, n, None) == -8
+    Zh = np.zeros((n, 2), order="F")
+    assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, 2, 0, lam.data_ptr(), Z.data_ptr(), Zh.ctypes.data, n,
+                          None) == -9
+    assert L.skew_eig_bse(c.h, n, M.data_ptr(), n, 2, 0, lam.data_ptr(), Z.data_ptr(), Z.data_ptr() + 16 * n, 7,
+                          None) == -10
+
 
 
 def test_bse_stage_bad_arguments(sk):

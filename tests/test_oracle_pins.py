@@ -517,6 +517,7 @@ def test_bse_hbs_eig_vs_brute_force(n):
     assert np.max(np.abs(lam - ref)) <= 1e-12 * nH
     r = np.linalg.norm(H @ X - X * lam, axis=0) / np.linalg.norm(X, axis=0)
     assert r.max() <= 1e-12 * nH
+    assert np.max(np.abs(np.linalg.norm(X, axis=0) - 1.0)) <= 1e-13   # unit 2-norm
     # the paired eigenvalue -lam has eigenvector [B-bar x2... ]: the H_BS structure maps
     # x = [u; v] to [v-bar; u-bar] with eigenvalue -lam
     Xp = np.vstack([X[n:].conj(), X[:n].conj()])
