@@ -430,7 +430,8 @@ struct BT2Cfg {
   static constexpr int XS = NB * LDX, GS = Gp::ELEMS;
   static constexpr size_t SMEM = (size_t)(XS + 2 * GS) * sizeof(double) + 6 * sizeof(uint64_t);
   static_assert(LDX % 16 == 4, "pad");
-  static_assert(RING % 64 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && K2 == 32 && (NB == 64 || NB == 32),
+  static_assert(RING % 32 == 0 && RW % 8 == 0 && RING >= RW + BB && BB == 64 && K2 == 32 &&
+                    (NB == 96 || NB == 64 || NB == 32),
                 "ring");
 };
 
@@ -684,9 +685,10 @@ __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_
         pub_rend = pblk * K2 + pt * BB + (pfinal ? RW : BB);
       }
       bool stored = false;
-      if (has_next && nblk_ != blk && (ntask_of(blk) == 1 || nsplit > 1)) {
+      if (has_next && nblk_ != blk && (ntask_of(blk) == 1 || nsplit > 1 || RING < 2 * RW)) {
         if (pub_blk >= 0) { publish(pub_blk, pub_rend); pub_blk = -1; }
-        // the next block's first window overlaps this single-step block's window -- or, in
+        // the next block's first window overlaps this block's last window (a single-step block,
+        // or a ring shorter than two windows: RING = RW + BB) -- or, in
         // the wavefront, the partner CTA needs this block's last rows before it can publish
         // the rows our next block waits for: wait for step q and write it back before loading
         mbar_wait(&empty[q & 1], (unsigned)((q >> 1) & 1));
@@ -861,9 +863,13 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
   return cudaGetLastError();
 }
 
-static constexpr double kNB32Cost = 0.55;   // per-strip time of a 32-wide strip / a 64-wide one
+// per-strip time of a 96- / 32-wide strip relative to a 64-wide one (tools/bt2_time.py)
+static constexpr double kNB96Cost = 1.5, kNB32Cost = 0.55;
 
-static constexpr int kBT2K2 = 32, kBT2RW = 96, kBT2Ring = 192, kBT2BB = 64;
+// ring of RW + BB rows: within a sweep block step q+1's new rows reuse step q-1's leaving
+// rows; at a block boundary the producer writes the last window back before loading the
+// next block's (one stalled step per block, ~n/64 steps)
+static constexpr int kBT2K2 = 32, kBT2RW = 96, kBT2Ring = 160, kBT2BB = 64;
 
 // [U | V] blocks of every group (depends only on the chase output: the solve driver runs it
 // on an auxiliary stream, concurrently with the tridiagonal solve)
@@ -898,31 +904,42 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t s64 = (ncols + 63) / 64;
-  int64_t n64 = s64;
+  // strip mix: a96 x 96 + a64 x 64 + the rest in 32-wide strips; each width is one launch
+  // and each launch costs (#waves) x (its strip time)
+  int64_t n96 = 0, n64 = 0;
   double best = 1e300;
-  for (int64_t a64 = 0; a64 <= s64; a64++) {
-    const int64_t rest = std::max<int64_t>(0, ncols - 64 * a64);
-    const int64_t a32 = (rest + 31) / 32;
-    const double tw = (double)((a64 + nsm - 1) / nsm) + kNB32Cost * (double)((a32 + nsm - 1) / nsm);
-    if (tw < best - 1e-9) { best = tw; n64 = a64; }
+  for (int64_t a96 = 0; a96 <= (ncols + 95) / 96; a96++) {
+    const int64_t r1 = std::max<int64_t>(0, ncols - 96 * a96);
+    for (int64_t a64 = 0; a64 <= (r1 + 63) / 64; a64++) {
+      const int64_t r2 = std::max<int64_t>(0, r1 - 64 * a64);
+      const int64_t a32 = (r2 + 31) / 32;
+      const double tw = kNB96Cost * (double)((a96 + nsm - 1) / nsm) + (double)((a64 + nsm - 1) / nsm) +
+                        kNB32Cost * (double)((a32 + nsm - 1) / nsm);
+      if (tw < best - 1e-9) { best = tw; n96 = a96; n64 = a64; }
+    }
   }
   // Wavefront option: all strips 64 wide, each walked by TWO CTAs that take alternate sweep
   // blocks (the kernel's nsplit; 16-byte aligned X only).  Correct (bit-identical) but not
-  // yet faster than the 64/32 mix: 4096 columns at n = 32768 take 671 ms split vs 589 ms in
-  // 32-wide strips (tools/bt2_time.py), so it is only enabled by SKEWEIG_BT2_SPLIT=2.
+  // yet faster than the strip mix: 4096 columns at n = 32768 take 671 ms split vs 589 ms in
+  // 32-wide strips (tools/bt2_time.py, round 1), so it is only enabled by SKEWEIG_BT2_SPLIT=2.
   const bool xvec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
   int nsplit = 1;
   if (const char* v = getenv("SKEWEIG_BT2_SPLIT")) nsplit = (atoi(v) == 2 && xvec && w.prog) ? 2 : 1;   // experiments
-  if (nsplit == 2) n64 = s64;
-  if (const char* v = getenv("SKEWEIG_BT2_NB")) n64 = (atoi(v) == 32) ? 0 : s64;   // experiments
-  if (n64 != s64) nsplit = 1;
-  const int64_t c64 = std::min<int64_t>(ncols, 64 * n64), c32 = ncols - c64;
+  if (nsplit == 2) { n96 = 0; n64 = (ncols + 63) / 64; }
+  if (const char* v = getenv("SKEWEIG_BT2_NB")) {   // experiments: one strip width only
+    const int wv = atoi(v);
+    n96 = (wv == 96) ? (ncols + 95) / 96 : 0;
+    n64 = (wv == 64) ? (ncols + 63) / 64 : 0;
+  }
+  if (n96 != 0 || n64 != (ncols + 63) / 64) nsplit = 1;
+  const int64_t c96 = std::min<int64_t>(ncols, 96 * n96);
+  const int64_t c64 = std::min<int64_t>(ncols - c96, 64 * n64);
+  const int64_t c32 = ncols - c96 - c64;
   int gskew = 0;
   if (const char* v = getenv("SKEWEIG_BT2_SKEW")) gskew = atoi(v);   // experiments
   auto launch = [&](auto kern, size_t smem, int NBv, int64_t cbeg, int64_t cnt, int ns) -> cudaError_t {
     if (cnt <= 0) return cudaSuccess;
-    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e2 = set_smem_attr((const void*)kern, (int)smem);
     if (e2) return e2;
     const int64_t grid = ((cnt + NBv - 1) / NBv) * ns;
     if (ns > 1) {
@@ -930,19 +947,18 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
       if (e2) return e2;
     }
     KScope ks(KC_BT2, st);
-    kern<<<(unsigned)grid, 32 * (NBv / 8 + 4), smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp, ns, w.prog,
-                                            gskew);
+    kern<<<(unsigned)grid, 32 * (NBv / 8 + 4), smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp,
+                                                           ns, w.prog, gskew);
     return cudaGetLastError();
   };
-  if (nsplit > 1)
-    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, true>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64, 0,
-               c64, nsplit);
-  else
-    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, false>, BT2Cfg<64, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 64,
-               0, c64, 1);
+  e = launch(bt2_ws_kernel<96, K2, RW, RING, BB, false>, BT2Cfg<96, K2, RW, RING, BB>::SMEM, 96, 0, c96, 1);
   if (e) return e;
-  e = launch(bt2_ws_kernel<32, K2, RW, RING, BB, false>, BT2Cfg<32, K2, RW, RING, BB>::SMEM + 2 * sizeof(uint64_t), 32,
-             c64, c32, 1);
+  if (nsplit > 1)
+    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, true>, BT2Cfg<64, K2, RW, RING, BB>::SMEM, 64, c96, c64, nsplit);
+  else
+    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, false>, BT2Cfg<64, K2, RW, RING, BB>::SMEM, 64, c96, c64, 1);
+  if (e) return e;
+  e = launch(bt2_ws_kernel<32, K2, RW, RING, BB, false>, BT2Cfg<32, K2, RW, RING, BB>::SMEM, 32, c96 + c64, c32, 1);
   if (e) return e;
   if (dbgp) {
     long long h[6];

@@ -24,7 +24,7 @@ ctx.set_profiling(True)
 for nc in cols:
     X0 = torch.randn((nc, n), dtype=torch.float64, device="cuda").t()   # column-major n x nc
     out = {}
-    for nbw in ("auto", "64", "32"):
+    for nbw in ("auto", "96", "64", "32"):
         if nbw == "auto":
             os.environ.pop("SKEWEIG_BT2_NB", None)
         else:
@@ -39,5 +39,5 @@ for nc in cols:
         out[nbw] = X
         flops = 4.0 * n * n * nc * 32 / 64 * (96 / 32)   # rough: 2 GEMMs of RW x K2 x NB per step
         print(f"n={n} ncols={nc} NB={nbw}: bt2 {best:.1f} ms", flush=True)
-    d = max((out["64"] - out["32"]).abs().max().item(), (out["64"] - out["auto"]).abs().max().item())
-    print(f"n={n} ncols={nc} max|X64-X32|, |X64-Xauto| = {d:.2e}", flush=True)
+    d = max((out["64"] - out[k]).abs().max().item() for k in ("32", "96", "auto"))
+    print(f"n={n} ncols={nc} max|X64 - X(32, 96, auto)| = {d:.2e}", flush=True)
