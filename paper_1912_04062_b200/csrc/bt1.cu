@@ -11,6 +11,7 @@
 //     X  -= V_g Z          (n_g x 2nev)   DMMA GEMM
 #include "common.cuh"
 #include "gemm_dmma.cuh"
+#include "tma_gemm.cuh"
 #include "internal.h"
 #include <algorithm>
 #include <vector>
@@ -147,6 +148,9 @@ cudaError_t bt1_apply(const F2BLayout& L, const double* vstore, const double* ta
   const int b = L.b;
   const int K = L.merge * b;
   if (L.ngroup == 0) return cudaSuccess;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   for (int64_t g = L.ngroup - 1; g >= 0; g--) {
     const int64_t r0 = L.r0(g * L.merge);
     const int64_t m = L.n - r0;
@@ -170,7 +174,8 @@ cudaError_t bt1_apply(const F2BLayout& L, const double* vstore, const double* ta
       GemmArgs ga;
       ga.M = K; ga.N = ncols; ga.K = m;
       ga.A = w.U; ga.lda = ldu; ga.B = Xr; ga.ldb = ldx; ga.C = w.Z; ga.ldc = K; ga.alpha = 1.0; ga.beta = 0.0;
-      e = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
+      e = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 16, 6, true, false, false, false>(ga, nsm, st);
+      if (e == cudaErrorNotSupported) e = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
       if (e) return e;
     }
     // X[r0:, :] -= V Z
@@ -179,7 +184,8 @@ cudaError_t bt1_apply(const F2BLayout& L, const double* vstore, const double* ta
       GemmArgs ga;
       ga.M = m; ga.N = ncols; ga.K = K;
       ga.A = V; ga.lda = ldv; ga.B = w.Z; ga.ldb = K; ga.C = Xr; ga.ldc = ldx; ga.alpha = -1.0; ga.beta = 1.0;
-      e = gemm_dmma<64, 64, 16, 32, 32, 2, false, false, false>(ga, st);
+      e = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 16, 4, false, false, true, false>(ga, nsm, st);
+      if (e == cudaErrorNotSupported) e = gemm_dmma<64, 64, 16, 32, 32, 2, false, false, false>(ga, st);
       if (e) return e;
     }
   }

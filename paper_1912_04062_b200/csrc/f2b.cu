@@ -12,6 +12,7 @@
 // skew matrix is never written and stays 0); the upper triangle is never read.
 #include "common.cuh"
 #include "gemm_dmma.cuh"
+#include "tma_gemm.cuh"
 #include "internal.h"
 #include <cooperative_groups.h>
 #include <algorithm>
@@ -817,6 +818,160 @@ __global__ void __launch_bounds__(GemmTile<BM, NB, BK, 32, 32, STAGES, false, fa
   }
 }
 
+// ---- a3 skew-SYMM, one device, TMA-fed persistent version --------------------------------
+// Work unit (p, piece): a contiguous range [v0, v1) of row block p's "virtual" K sequence --
+// the kr = (p+1) BM/BK k-blocks of the row part L[p, 0:(p+1)BM] U followed by the kc k-blocks
+// of the column part -L[pBM:m, p]^T U.  kr + kc = (nt + 1) BM / BK is the same for every p,
+// so all units are equal.  The producer warp streams each k-block as one TMA box of S (row
+// part: box (BM+4) x BK, M-major; column part: box (BK+4) x BM of the transposed region,
+// K-major) plus one box of U; the consumers run the matching GemmTile fragment loop, with
+// the strictly-lower mask applied to the A fragments of the diagonal k-blocks in registers.
+template <int BM, int BK>
+struct SymmTma {
+  using TR = GemmTile<BM, 64, BK, 32, 32, 2, false, false>;   // row part: A(m, k) = S[m0+m, k0+k]
+  using TC = GemmTile<BM, 64, BK, 32, 32, 2, true, false>;    // col part: A(m, k) = S[k0+k, m0+m]
+  static constexpr int NCW = TR::NTHREADS / 32;
+  static constexpr int THREADS = TR::NTHREADS + 32;
+  static constexpr int A_ST = (TR::A_STAGE > TC::A_STAGE ? TR::A_STAGE : TC::A_STAGE);
+  static constexpr int B_ST = TR::B_STAGE;
+  static constexpr int NS = 4;
+  static constexpr size_t SMEM = (size_t)NS * (A_ST + B_ST) * sizeof(double) + 2 * NS * 8 + 128;
+  static constexpr unsigned AR_BYTES = (unsigned)(TR::A_STAGE * 8), AC_BYTES = (unsigned)(TC::A_STAGE * 8);
+  static constexpr unsigned B_BYTES = (unsigned)(B_ST * 8);
+  static_assert(TR::B_STAGE == TC::B_STAGE && (A_ST * 8) % 128 == 0 && (B_ST * 8) % 128 == 0, "symm tma layout");
+};
+
+struct SymmTmaArgs {
+  int64_t m, nt;
+  int split;
+  double* out; int64_t ldo;     // split == 1: X; else Ycol (piece k at out + k*ldo*64)
+};
+
+// mma_stage with the strictly-lower mask of S on the A fragments: keep A(m, k) iff its S row
+// index exceeds its S column index; row part: m0 + m > k0 + k, column part: k0 + k > m0 + m.
+template <class T, bool ROWPART>
+__device__ __forceinline__ void symm_stage_masked(const double* As, const double* Bs, double (&acc)[T::FM][T::FN][2],
+                                                  int wm0, int wn0, int lane, int dk /* k0 - m0 */) {
+  const int gq = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < T::BK_; kk += 4) {
+    double af[T::FM], bf[T::FN];
+#pragma unroll
+    for (int i = 0; i < T::FM; i++) {
+      const int mm = wm0 + 8 * i + gq, kx = kk + t;
+      const double a = T::a_at(As, mm, kx);
+      const bool keep = ROWPART ? (mm > kx + dk) : (kx + dk > mm);
+      af[i] = keep ? a : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < T::FN; j++) bf[j] = T::b_at(Bs, kk + t, wn0 + 8 * j + gq);
+#pragma unroll
+    for (int i = 0; i < T::FM; i++)
+#pragma unroll
+      for (int j = 0; j < T::FN; j++) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+}
+
+template <int BM, int BK>
+__global__ void __launch_bounds__(SymmTma<BM, BK>::THREADS, 1)
+    symm_tma_kernel(const __grid_constant__ CUtensorMap mapR, const __grid_constant__ CUtensorMap mapC,
+                    const __grid_constant__ CUtensorMap mapU, SymmTmaArgs a) {
+  using Cfg = SymmTma<BM, BK>;
+  using TR = typename Cfg::TR;
+  using TC = typename Cfg::TC;
+  constexpr int NS = Cfg::NS, KPB = BM / BK;
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+  double* As = sm;
+  double* Bs = As + NS * Cfg::A_ST;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + NS * Cfg::B_ST);
+  uint64_t* empty = full + NS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NS; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], Cfg::NCW); }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t nunits = a.nt * a.split;
+  const int64_t kv = (a.nt + 1) * KPB;   // virtual k-blocks per row block (all equal)
+  if (warp == Cfg::NCW) {
+    // ================================ producer ================================
+    if (lane == 0) {
+      tma_prefetch_desc(&mapR);
+      tma_prefetch_desc(&mapC);
+      tma_prefetch_desc(&mapU);
+      int64_t it = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t p = u / a.split, k = u % a.split;
+        const int64_t kr = (p + 1) * KPB;
+        const int64_t v0 = (kv * k) / a.split, v1 = (kv * (k + 1)) / a.split;
+        const int m0 = (int)(p * BM);
+        for (int64_t v = v0; v < v1; v++, it++) {
+          const int s = (int)(it % NS);
+          mbar_wait(&empty[s], (unsigned)(((it / NS) & 1) ^ 1));
+          const bool row = v < kr;
+          const int k0 = row ? (int)(v * BK) : (int)(m0 + (v - kr) * BK);
+          mbar_expect_tx(&full[s], (row ? Cfg::AR_BYTES : Cfg::AC_BYTES) + Cfg::B_BYTES);
+          if (row) tma_load_2d(As + s * Cfg::A_ST, &mapR, m0, k0, &full[s]);
+          else tma_load_2d(As + s * Cfg::A_ST, &mapC, k0, m0, &full[s]);
+          tma_load_2d(Bs + s * Cfg::B_ST, &mapU, k0, 0, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  // ================================ consumers ================================
+  const int wm0 = (warp % TR::NWARP_M) * 32, wn0 = (warp / TR::NWARP_M) * 32;
+  const int gq = lane >> 2, tq = lane & 3;
+  int64_t it = 0;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t p = u / a.split, k = u % a.split;
+    const int64_t kr = (p + 1) * KPB;
+    const int64_t v0 = (kv * k) / a.split, v1 = (kv * (k + 1)) / a.split;
+    const int64_t m0 = p * BM;
+    double acc[TR::FM][TR::FN][2];
+#pragma unroll
+    for (int i = 0; i < TR::FM; i++)
+#pragma unroll
+      for (int j = 0; j < TR::FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int64_t v = v0; v < v1; v++, it++) {
+      const int s = (int)(it % NS);
+      mbar_wait(&full[s], (unsigned)((it / NS) & 1));
+      const double* Ast = As + s * Cfg::A_ST;
+      const double* Bst = Bs + s * Cfg::B_ST;
+      if (v < kr) {
+        const int64_t k0 = v * BK;
+        if (k0 + BK > m0) symm_stage_masked<TR, true>(Ast, Bst, acc, wm0, wn0, lane, (int)(k0 - m0));
+        else TR::mma_stage(Ast, Bst, acc, wm0, wn0, lane);
+      } else {
+        if (v == kr) {   // entering the column part: acc <- -acc, accumulate L^T U, negate at the end
+#pragma unroll
+          for (int i = 0; i < TR::FM; i++)
+#pragma unroll
+            for (int j = 0; j < TR::FN; j++) { acc[i][j][0] = -acc[i][j][0]; acc[i][j][1] = -acc[i][j][1]; }
+        }
+        const int64_t k0 = m0 + (v - kr) * BK;
+        if (k0 < m0 + BM) symm_stage_masked<TC, false>(Ast, Bst, acc, wm0, wn0, lane, (int)(k0 - m0));
+        else TC::mma_stage(Ast, Bst, acc, wm0, wn0, lane);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    const double sg = (v1 > kr) ? -1.0 : 1.0;   // row - col
+    double* out = a.out + (size_t)k * a.ldo * 64;
+#pragma unroll
+    for (int i = 0; i < TR::FM; i++)
+#pragma unroll
+      for (int j = 0; j < TR::FN; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int64_t mm = m0 + wm0 + 8 * i + gq;
+          const int nn = wn0 + 8 * j + 2 * tq + h;
+          if (mm < a.m) out[SK_IDX(mm, nn, a.ldo)] = sg * acc[i][j][h];
+        }
+  }
+}
+
 // X = sum_k Ycol[k] (single-device split-K skew-SYMM; fixed order)
 __global__ void symm_sum_kernel(double* X, int64_t ldx, const double* Ycol, int64_t ldy, int npieces, int64_t m) {
   const int64_t col = blockIdx.y;
@@ -1029,6 +1184,46 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
   return e;
 }
 
+// single-device skew-SYMM X = S U on the TMA-fed persistent kernel (128-row blocks, equal
+// units, split-K pieces summed in a fixed order); cudaErrorNotSupported -> caller falls back
+static cudaError_t symm_tma(const double* S, int64_t lds, const double* U, int64_t ldu, double* X, int64_t ldx,
+                            int64_t m, double* Ycol, int nsm, cudaStream_t st) {
+  constexpr int BM = 128, BK = 16;
+  using Cfg = SymmTma<BM, BK>;
+  if (m < 1 || !tma_ptr_ok(S, lds) || !tma_ptr_ok(U, ldu) || tma_encode_fn() == nullptr) return cudaErrorNotSupported;
+  CUtensorMap mR, mC, mU;
+  if (!tma_map_2d(&mR, S, m, m, lds, BM + 4, BK) || !tma_map_2d(&mC, S, m, m, lds, BK + 4, BM) ||
+      !tma_map_2d(&mU, U, m, 64, ldu, BK + 4, 64))
+    return cudaErrorNotSupported;
+  const int64_t nt = (m + BM - 1) / BM;
+  // pieces per row block: best wave efficiency (units / (waves * SMs)), small cost per piece
+  int split = 1;
+  double best = -1e300;
+  for (int c = 1; c <= kSymmMaxSplit; c++) {
+    const int64_t units = nt * c;
+    const int64_t waves = (units + nsm - 1) / nsm;
+    const double eff = (double)units / (double)(waves * nsm) - 0.01 * (c - 1);
+    if (eff > best + 1e-12) { best = eff; split = c; }
+  }
+  SymmTmaArgs a;
+  a.m = m; a.nt = nt; a.split = split;
+  a.out = split > 1 ? Ycol : X;
+  a.ldo = split > 1 ? ldx : ldx;
+  cudaError_t e = set_smem_attr((const void*)symm_tma_kernel<BM, BK>, (int)Cfg::SMEM);
+  if (e) return e;
+  KScope ks(KC_SYMM, st, split > 1 ? 2 : 1);
+  const int grid = (int)std::min<int64_t>(nt * split, nsm);
+  symm_tma_kernel<BM, BK><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(mR, mC, mU, a);
+  e = cudaGetLastError();
+  if (e) return e;
+  if (split > 1) {
+    dim3 cg((unsigned)std::min<int64_t>((m + 255) / 256, 64), 64u);
+    symm_sum_kernel<<<cg, 256, 0, st>>>(X, ldx, Ycol, ldx, split, m);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
 cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, double* vstore, const F2BWork& w,
                        int nsm, cudaStream_t st, const Dist& d, int* nccl_err) {
   // distributed: trailing column block q (global block j+1+q) is local iff (j+1+q) mod P == rank
@@ -1051,7 +1246,13 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     e = gemm_dmma<64, 64, 16, 32, 32, 2, false, false, false>(ga, st);
     if (e) return e;
   }
-  {   // X = S U  -> P[:, b:2b]
+  bool symm_done = false;
+  if (d.P == 1 && b == 64 && !tma_disabled()) {   // X = S U -> P[:, b:2b], TMA-fed persistent kernel
+    e = symm_tma(S, lda, w.U, ldn, Wp, ldn, m, w.Ycol, nsm, st);
+    if (e == cudaSuccess) symm_done = true;
+    else if (e != cudaErrorNotSupported) return e;
+  }
+  if (!symm_done) {   // X = S U  -> P[:, b:2b]
     SymmArgs s;
     s.S = S; s.lds = lda; s.U = w.U; s.ldu = ldn; s.X = Wp; s.ldx = ldn; s.m = m; s.nb = b;
     s.vec = gemm_vec_ok(S, lda, w.U, ldn) ? 1 : 0;
@@ -1143,7 +1344,10 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
   }
   {
     KScope ks(KC_R2K, st);
-    e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
+    e = cudaErrorNotSupported;
+    if (ga.col_stride == 1 && !tma_disabled())   // one device: persistent TMA-fed 128 x 64 tiles
+      e = tma_gemm<128, 64, 16, 4, false, true, true, true>(ga, nsm, st);
+    if (e == cudaErrorNotSupported) e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
   }
   if (e) return e;
   return cudaGetLastError();

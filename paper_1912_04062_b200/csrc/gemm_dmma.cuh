@@ -43,6 +43,7 @@ struct GemmTile {
   static constexpr int NWARP_M = BM / WM, NWARP_N = BN / WN;
   static constexpr int NTHREADS = 32 * NWARP_M * NWARP_N;
   static constexpr int FM = WM / 8, FN = WN / 8;             // 8x8 fragments per warp
+  static constexpr int BK_ = BK;
   // shared layouts
   static constexpr int A_LD = A_KMAJ ? (BK + 4) : (BM + 4);
   static constexpr int A_ROWS = A_KMAJ ? BM : BK;

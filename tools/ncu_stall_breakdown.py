@@ -8,9 +8,13 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
-if len(sys.argv) > 2:
-    cmd += ["-k", "regex:" + sys.argv[2]]
+sub = sys.argv[2] if len(sys.argv) > 2 else None   # substring of the kernel name (last match)
 rows = list(csv.reader(io.StringIO(subprocess.run(cmd, capture_output=True, text=True).stdout)))
+if sub:   # keep the rows of the last block whose "Kernel Name" contains sub
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name" and sub in r[1]]
+    i0 = starts[-1]
+    nxt = [i for i, r in enumerate(rows) if i > i0 and r and r[0] == "Kernel Name"]
+    rows = rows[i0:(nxt[0] if nxt else len(rows))]
 hdr = next(r for r in rows if r and r[0] == "Address")
 data = [r for r in rows if r and r[0].startswith("0x")]
 si = {h: i for i, h in enumerate(hdr)}
