@@ -91,6 +91,18 @@ int skew_ctx_destroy(skew_ctx ctx);
 int skew_get_unique_id(char id[128]);
 int skew_ctx_create_dist(skew_ctx* out, int device, void* cuda_stream, int nranks, int rank, const char id[128]);
 
+/* Virtual ranks (test harness for the distributed path on ONE device): skew_vgroup_create
+ * makes a group of nranks; skew_ctx_create_virtual makes the context of rank `rank` in it
+ * (all on `device`).  Each rank's solve must be called from its own host thread (the
+ * collectives meet at host barriers; the contexts may share one stream).  The distributed
+ * algorithm is the one of skew_ctx_create_dist (same ownership, partitions, ghost windows);
+ * the collectives are device copies and a fixed-order sum kernel that read the peers'
+ * buffers.  The group allocates its own reduction scratch (cudaMalloc) and must outlive its
+ * contexts.  Returns -i for a bad argument i. */
+int skew_vgroup_create(int nranks, void** out);
+int skew_vgroup_destroy(void* group);
+int skew_ctx_create_virtual(skew_ctx* out, int device, void* cuda_stream, void* group, int nranks, int rank);
+
 /* Bytes of device workspace a solve of order n with nev pairs needs (flags:
  * SKEW_WS_*).  The caller allocates it (e.g. a torch uint8 tensor) and passes it
  * with skew_set_workspace; it must stay alive while the context uses it. */

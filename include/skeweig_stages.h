@@ -47,6 +47,14 @@ int skew_set_profiling(skew_ctx ctx, int on);
 int skew_kernel_stats(skew_ctx ctx, double* ms_out, int64_t* launches_out, int count);
 const char* skew_kernel_class_name(int cls);
 
+/* The rank-2k update's lower-triangular tile schedule (host function, no GPU needed):
+ * fills tm_out / tn_out (capacity cap) with the (row tile, column tile) pairs the
+ * skew rank-2k kernel of rank `rank` of `nranks` visits on a trailing matrix of ntm x ntm
+ * tiles (64 x 64 tiles, 1D block-cyclic column ownership rank(q) = (q - qoff) mod nranks
+ * with qoff = 0 here), in launch order.  Returns the count (or -i for a bad argument i).
+ * Tests check that the ranks' sets partition the lower triangle (tests/test_tile_schedule.py). */
+int64_t skew_tile_schedule(int64_t ntm, int nranks, int rank, int64_t* tm_out, int64_t* tn_out, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,7 @@ column-major layout the C-ABI takes).
 import ctypes
 import os
 
-__all__ = ["lib", "Context", "skew_eig", "skew_eig_range", "skew_eig_host_range", "skew_eigvals", "skew_eig_bse", "bse_hbs_eig", "skew_eig_host",
+__all__ = ["lib", "Context", "VirtualGroup", "skew_eig", "skew_eig_range", "skew_eig_host_range", "skew_eigvals", "skew_eig_bse", "bse_hbs_eig", "skew_eig_host",
            "reduce_to_band", "band_to_tridiag", "tridiag_eig", "expand_half_spectrum", "SkewError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -41,6 +41,11 @@ EXPORTS = {
     "skew_get_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "skew_ctx_create_dist": ([ctypes.POINTER(_vp), ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p],
                              ctypes.c_int),
+    "skew_tile_schedule": ([_i64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, _i64], _i64),
+    "skew_vgroup_create": ([ctypes.c_int, ctypes.POINTER(_vp)], ctypes.c_int),
+    "skew_vgroup_destroy": ([_vp], ctypes.c_int),
+    "skew_ctx_create_virtual": ([ctypes.POINTER(_vp), ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int],
+                                ctypes.c_int),
     "skew_workspace_size": ([_vp, _i64, _i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "skew_set_workspace": ([_vp, _vp, ctypes.c_size_t], ctypes.c_int),
     "skew_eig": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
@@ -95,19 +100,47 @@ def _torch():
     return torch
 
 
+class VirtualGroup:
+    """A group of P virtual ranks on one device (skew_vgroup_create): Context(virtual=(g, r))
+    makes rank r's context.  Test harness for the distributed path on a single GPU; each
+    rank's solve runs in its own host thread (the collectives meet at host barriers)."""
+
+    def __init__(self, nranks):
+        h = _vp()
+        rc = lib().skew_vgroup_create(nranks, ctypes.byref(h))
+        if rc != 0:
+            raise SkewError(rc, "skew_vgroup_create failed")
+        self.h, self.nranks = h, nranks
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().skew_vgroup_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class Context:
     """One C-ABI context per (device, stream) plus a torch-allocated device workspace."""
 
-    def __init__(self, device=None, stream=None, group=None, distributed=False):
+    def __init__(self, device=None, stream=None, group=None, distributed=False, virtual=None):
         """distributed=True: a collective context over torch.distributed `group` (NCCL inside the
-        library; the unique id is exchanged with broadcast_object_list)."""
+        library; the unique id is exchanged with broadcast_object_list).  virtual=(VirtualGroup,
+        rank): rank `rank` of a virtual-rank group on this device."""
         torch = _torch()
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    torch.device(device).index or 0)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         h = _vp()
-        if distributed:
+        if virtual is not None:
+            vg, rank = virtual
+            self._vg = vg   # the group must outlive the context
+            rc = lib().skew_ctx_create_virtual(ctypes.byref(h), self.device.index, _vp(self.stream.cuda_stream), vg.h,
+                                               vg.nranks, rank)
+            self.rank, self.world = rank, vg.nranks
+        elif distributed:
             import torch.distributed as dist
             rank, world = dist.get_rank(group), dist.get_world_size(group)
             buf = ctypes.create_string_buffer(128)

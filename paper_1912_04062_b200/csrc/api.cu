@@ -6,6 +6,7 @@
 #include "../../include/skeweig_stages.h"
 #include "common.cuh"
 #include "internal.h"
+#include "gemm_dmma.cuh"
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
@@ -196,6 +197,57 @@ int skew_ctx_create_dist(skew_ctx* out, int device, void* cuda_stream, int nrank
   return SKEW_OK;
 }
 
+int64_t skew_tile_schedule(int64_t ntm, int nranks, int rank, int64_t* tm_out, int64_t* tn_out, int64_t cap) {
+  if (ntm < 0) return -1;
+  if (nranks < 1) return -2;
+  if (rank < 0 || rank >= nranks) return -3;
+  if (cap < 0 || ((!tm_out || !tn_out) && cap > 0)) return -6;
+  // the same grid size and tile decoding as gemm_dmma<..., TRI> (gemm_dmma.cuh)
+  int64_t cnt;
+  if (nranks > 1) {
+    const int64_t off = rank, st = nranks;
+    if (off >= ntm) return 0;
+    const int64_t kmax = (ntm - off + st - 1) / st;
+    cnt = kmax * (ntm - off) - st * kmax * (kmax - 1) / 2;
+  } else {
+    cnt = ntm * (ntm + 1) / 2;
+  }
+  for (int64_t t = 0; t < cnt && t < cap; t++) {
+    int64_t tm, tn;
+    if (nranks > 1) tri_tile_strided(t, ntm, nranks, rank, tm, tn);
+    else tri_tile(t, 1, tm, tn);
+    tm_out[t] = tm;
+    tn_out[t] = tn;
+  }
+  return cnt;
+}
+
+int skew_vgroup_create(int nranks, void** out) {
+  if (nranks < 1) return -1;
+  if (!out) return -2;
+  *out = vgroup_new(nranks);
+  return SKEW_OK;
+}
+
+int skew_vgroup_destroy(void* group) {
+  if (!group) return -1;
+  vgroup_free(static_cast<VGroup*>(group));
+  return SKEW_OK;
+}
+
+int skew_ctx_create_virtual(skew_ctx* out, int device, void* cuda_stream, void* group, int nranks, int rank) {
+  if (!out) return -1;
+  if (!group) return -4;
+  if (nranks < 1) return -5;
+  if (rank < 0 || rank >= nranks) return -6;
+  int rc = skew_ctx_create(out, device, cuda_stream);
+  if (rc != SKEW_OK) return rc;
+  (*out)->c.nranks = nranks;
+  (*out)->c.rank = rank;
+  (*out)->c.vg = static_cast<VGroup*>(group);
+  return SKEW_OK;
+}
+
 int skew_ctx_destroy(skew_ctx ctx) {
   if (!ctx) return -1;
   if (ctx->c.nccl) ncclCommDestroy((ncclComm_t)ctx->c.nccl);
@@ -311,7 +363,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   // ---- full -> band
   tstart(ctx, ST_F2B);
   Dist d;
-  d.P = c.nranks; d.rank = c.rank; d.comm = c.nccl;
+  d.P = c.nranks; d.rank = c.rank; d.comm = c.nccl; d.vg = c.vg;
   if (d.P > 1 && !getenv("SKEWEIG_NO_LOOKAHEAD")) {   // env: experiments only
     d.aux = c.aux; d.ev_cols = c.ev_la_cols; d.ev_panel = c.ev_la_panel;
   }
@@ -319,7 +371,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
     CK(cudaMemsetAsync(p.vstore, 0, sizeof(double) * p.f2b.vstore_elems, st), "memset vstore");
     int nerr = 0;
     cudaError_t fe = f2b_run(p.f2b, A_d, lda, p.vstore, p.fw, c.num_sms, st, d, &nerr);
-    if (nerr) { c.last_error = std::string("f2b: NCCL ") + ncclGetErrorString((ncclResult_t)nerr); return SKEW_ERR_NCCL; }
+    if (nerr) { c.last_error = std::string("f2b: ") + coll_error_string(d, nerr); return SKEW_ERR_NCCL; }
     CK(fe, "f2b");
   }
   tstop(ctx, ST_F2B);
@@ -327,8 +379,8 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   tstart(ctx, ST_B2T);
   CK(band_extract(A_d, lda, n, c.prm.b, p.bw.AB, p.b2t.ldab, st, d.P, d.rank), "band extract");
   if (d.P > 1) {   // every rank contributed the band columns it owns
-    ncclResult_t r = ncclAllReduce(p.bw.AB, p.bw.AB, (size_t)p.b2t.ldab * n, ncclDouble, ncclSum, (ncclComm_t)d.comm, st);
-    if (r != ncclSuccess) { c.last_error = std::string("band allreduce: NCCL ") + ncclGetErrorString(r); return SKEW_ERR_NCCL; }
+    const int r = coll_allreduce_sum(d, p.bw.AB, (size_t)p.b2t.ldab * n, st);
+    if (r) { c.last_error = std::string("band allreduce: ") + coll_error_string(d, r); return SKEW_ERR_NCCL; }
   }
   CK(b2t_run(p.b2t, p.bw, p.alpha, c.num_sms, st), "b2t");
   tstop(ctx, ST_B2T);

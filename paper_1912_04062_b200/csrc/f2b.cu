@@ -1296,8 +1296,8 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     }
   }
   if (d.P > 1) {   // Y = sum over ranks of the partial skew-SYMM products (NVLink allreduce)
-    ncclResult_t r = ncclAllReduce(Wp, Wp, (size_t)ldn * b, ncclDouble, ncclSum, (ncclComm_t)d.comm, st);
-    if (r != ncclSuccess) { *nccl_err = (int)r; return cudaErrorUnknown; }
+    const int r = coll_allreduce_sum(d, Wp, (size_t)ldn * b, st);
+    if (r) { *nccl_err = r; return cudaErrorUnknown; }
   }
   {   // W = X - 1/2 V (T^T (V^T X));  P = [V W], Q = [W -V]
     KScope ks(KC_WCORR, st, 5);
@@ -1376,14 +1376,12 @@ cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, 
     if (d.P > 1) {
       const int64_t g = j / L.merge, pl = j % L.merge;
       double* Vcols = vstore + L.goff[g] + pl * (int64_t)L.b * L.gld[g];   // the panel's columns of the group block
-      ncclComm_t comm = (ncclComm_t)d.comm;
-      ncclResult_t r = ncclGroupStart();
-      if (r == ncclSuccess) r = ncclBroadcast(Vcols, Vcols, (size_t)L.gld[g] * L.b, ncclDouble, owner, comm, st);
-      if (r == ncclSuccess) r = ncclBroadcast(w.T + j * (int64_t)L.b * L.b, w.T + j * (int64_t)L.b * L.b,
-                                              (size_t)L.b * L.b, ncclDouble, owner, comm, st);
-      if (r == ncclSuccess) r = ncclBroadcast(w.tau + j * L.b, w.tau + j * L.b, (size_t)L.b, ncclDouble, owner, comm, st);
-      ncclResult_t r2 = ncclGroupEnd();
-      if (r != ncclSuccess || r2 != ncclSuccess) { *nccl_err = (int)(r != ncclSuccess ? r : r2); return cudaErrorUnknown; }
+      int r = coll_group_start(d);
+      if (!r) r = coll_bcast(d, Vcols, sizeof(double) * (size_t)L.gld[g] * L.b, owner, st);
+      if (!r) r = coll_bcast(d, w.T + j * (int64_t)L.b * L.b, sizeof(double) * (size_t)L.b * L.b, owner, st);
+      if (!r) r = coll_bcast(d, w.tau + j * L.b, sizeof(double) * (size_t)L.b, owner, st);
+      const int r2 = coll_group_end(d);
+      if (r || r2) { *nccl_err = r ? r : r2; return cudaErrorUnknown; }
     }
     e = f2b_update(L, j, A, lda, vstore, w, nsm, st, d, nccl_err);
     if (e) return e;

@@ -172,7 +172,7 @@ struct GemmTile {
 // Lower-triangular tile enumeration for BM = R * BN (R >= 1): row tile tm meets the
 // (strictly) lower triangle in column tiles tn = 0 .. R*(tm+1)-1; cumulative count
 // C(tm) = R * tm * (tm+1) / 2; t -> (tm, tn) with C(tm) <= t < C(tm+1).
-__device__ __forceinline__ void tri_tile(int64_t t, int R, int64_t& tm, int64_t& tn) {
+__host__ __device__ __forceinline__ void tri_tile(int64_t t, int R, int64_t& tm, int64_t& tn) {
   int64_t r = (int64_t)((sqrt(8.0 * (double)t / R + 1.0) - 1.0) * 0.5);
   while ((int64_t)R * (r + 1) * (r + 2) / 2 <= t) r++;
   while ((int64_t)R * r * (r + 1) / 2 > t) r--;
@@ -182,8 +182,8 @@ __device__ __forceinline__ void tri_tile(int64_t t, int R, int64_t& tm, int64_t&
 
 // Strided variant (BM == BN): column tiles tn_i = off + stride*i, rows tm in [tn_i, ntm);
 // S(k) = sum_{i<k} (ntm - tn_i) = k (ntm - off) - stride k (k-1) / 2.
-__device__ __forceinline__ void tri_tile_strided(int64_t t, int64_t ntm, int stride, int off, int64_t& tm,
-                                                 int64_t& tn) {
+__host__ __device__ __forceinline__ void tri_tile_strided(int64_t t, int64_t ntm, int stride, int off, int64_t& tm,
+                                                          int64_t& tn) {
   auto S = [&](int64_t k) -> int64_t { return k * (ntm - off) - (int64_t)stride * k * (k - 1) / 2; };
   const double A = 0.5 * stride, B = (double)(ntm - off) + 0.5 * stride;
   int64_t k = (int64_t)((B - sqrt(fmax(B * B - 4.0 * A * (double)t, 0.0))) / (2.0 * A));

@@ -26,6 +26,8 @@ struct Arena {
   }
 };
 
+struct VGroup;   // coll.cu: virtual-rank group
+
 struct Params {
   int b = 64;            // band width (F2B panel width), fixed
   int bt2_k = 32;        // BT2 group width (sweeps per group), SKEWEIG_BT2_K
@@ -51,6 +53,7 @@ struct Ctx {
   // distributed
   int nranks = 1, rank = 0;
   void* nccl = nullptr;
+  VGroup* vg = nullptr;   // virtual-rank group (not owned)
   // auxiliary stream: BT1 / BT2 preparation concurrent with the tridiagonal solve
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -187,16 +190,28 @@ struct BT1Work {
   int64_t* gmeta = nullptr;   // per group: V-store offset, ld, rows
 };
 
+// coll.cu: collectives over NCCL or over virtual ranks (P contexts on one device)
+VGroup* vgroup_new(int P);
+void vgroup_free(VGroup* g);
+
 // multi-GPU: 1D block-cyclic ownership of b-wide column blocks (owner of column c = (c / b) mod P)
 struct Dist {
   int P = 1, rank = 0;
   void* comm = nullptr;   // ncclComm_t
+  VGroup* vg = nullptr;   // virtual-rank group (instead of NCCL)
   // look-ahead (P > 1): the owner of panel j+1 factors it on `aux` (higher priority) while
   // its main stream finishes the rank-2k update of panel j on the other column blocks
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_cols = nullptr, ev_panel = nullptr;
 };
 
+// collectives (return 0 or a backend error code; see coll_error_string)
+int coll_bcast(const Dist& d, void* buf, size_t bytes, int root, cudaStream_t st);
+int coll_group_start(const Dist& d);
+int coll_group_end(const Dist& d);
+int coll_allreduce_sum(const Dist& d, double* buf, size_t count, cudaStream_t st);
+int coll_allgather(const Dist& d, double* buf, size_t count, cudaStream_t st);
+const char* coll_error_string(const Dist& d, int code);
 // f2b.cu
 void f2b_reserve(Arena& ar, const F2BLayout& L, int nsm, F2BWork& w, int P = 1);
 // returns cudaErrorUnknown + sets *nccl_err on an NCCL failure

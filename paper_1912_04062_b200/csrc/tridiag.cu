@@ -801,8 +801,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
       }
     }
     if (P > 1) {
-      ncclResult_t r = ncclAllGather(w.lamc + qa, w.lamc, (size_t)cnt, ncclDouble, (ncclComm_t)d->comm, st);
-      if (r != ncclSuccess) return cudaErrorUnknown;
+      if (coll_allgather(*d, w.lamc, (size_t)cnt, st)) return cudaErrorUnknown;
     }
     e = cudaMemcpyAsync(lamc.data(), w.lamc, sizeof(double) * ntask, cudaMemcpyDeviceToHost, st);
     if (e) return e;
