@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--seed", type=int, default=None)
     p.add_argument("--cpu-n", type=int, default=int(os.environ.get("BENCH_CPU_N", 4608)),
                    help="order of the bounded oracle sample (cpu_baseline / --impl reference)")
+    p.add_argument("--eigvals", action="store_true", help="eigenvalues only (skew_eigvals; BASELINE configs[4])")
+    p.add_argument("--regen", action="store_true",
+                   help="regenerate A on the device each step instead of copying a pristine copy (saves n^2 doubles)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile-json", default=None, help="write per-kernel stats here")
@@ -200,13 +203,20 @@ def run_ours(args):
     ctx = sk.Context(distributed=(ws > 1))   # collective context: distributed full->band over NCCL
     ctx.set_profiling(True)
     # pristine input (device generator, bit-identical to skewgen.random_skew)
-    A0 = torch.empty((n, n), dtype=torch.float64, device=dev).t()
-    skewgen.random_skew_lower_device(A0, n, seed, torch.cuda.current_stream().cuda_stream)
-    A = torch.empty_like(A0.t()).t()
+    A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+    A0 = None
+    if not args.regen:
+        A0 = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+        skewgen.random_skew_lower_device(A0, n, seed, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
 
     def step():
-        A.copy_(A0)
+        if A0 is None:   # the input is destroyed by each solve: regenerate it (inside the timed region)
+            skewgen.random_skew_lower_device(A, n, seed, torch.cuda.current_stream().cuda_stream)
+        else:
+            A.copy_(A0)
+        if args.eigvals:
+            return sk.skew_eigvals(A, nev, ctx=ctx, overwrite_a=True)
         return sk.skew_eig_range(A, nev, k0, k1, ctx=ctx, overwrite_a=True)
 
     for _ in range(args.warmup):
@@ -239,6 +249,8 @@ def run_ours(args):
         t_ms = tt.item()
         dist.barrier()
     fm = flop_model(n, nev)
+    if args.eigvals:   # eigenvalues only: the algorithmic work is the full->band reduction
+        fm = dict(fm, total=4.0 / 3.0 * n ** 3, bt1=0.0, bt2_apply=0.0)
     ms_step = t_ms / args.steps
     value = fm["total"] / (ms_step * 1e-3) / 1e12
     launches = sum(v[1] for v in kstats.values())
@@ -275,7 +287,7 @@ def run_ours(args):
 
     # ---------------- e2e: host buffers through the C-ABI (pinned host memory)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.eigvals and A0 is not None:
         Ah = torch.empty((n, n), dtype=torch.float64, pin_memory=True).t()
         Ah.copy_(A0)
         nloc = k1 - k0
@@ -313,7 +325,11 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms_step, "time_to_solution_s": ms_step / 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic: splitmix64 uniform[-1,1) strictly-lower skew, seed=n (DESIGN.md Input recipe)",
-                "config": {"workload": f"n={n} random skew, nev={nev} half spectrum (BASELINE configs[3])",
+                "config": {"workload": (f"n={n} random skew, eigenvalues only (nev={nev})" if args.eigvals else
+                                        f"n={n} random skew, nev={nev} half spectrum") +
+                                       (" (BASELINE configs[3])" if n == 32768 else
+                                        " (BASELINE configs[4])" if n == 65536 else ""),
+                           "memory_peak_gb_per_rank": torch.cuda.max_memory_allocated(dev) / 1e9,
                            "n": n, "nev": nev, "band": 64,
                            "parallelism": (f"full->band 1D block-cyclic over {ws} GPUs (NCCL bcast + allreduce); "
                                            f"bulge chasing replicated; eigenvectors sharded by range")

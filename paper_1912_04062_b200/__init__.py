@@ -284,13 +284,13 @@ def skew_eig_host_range(A_host, nev, k0, k1, lam_host, Zre_host, Zim_host, ctx=N
     return rc
 
 
-def skew_eigvals(A, nev=None, ctx=None):
+def skew_eigvals(A, nev=None, ctx=None, overwrite_a=False):
     """The nev largest lambda_k (descending) of the skew A (eigenvalues only)."""
     torch = _torch()
     c = _ctx(ctx)
     n = A.shape[0]
     nev = n // 2 if nev is None else nev
-    Ac = _colmajor(torch, A.to(device=c.device, dtype=torch.float64))
+    Ac = A if (overwrite_a and A.stride(0) == 1) else _colmajor(torch, A.to(device=c.device, dtype=torch.float64))
     c.ensure_workspace(n, nev, 0)
     lam = torch.empty(max(nev, 1), dtype=torch.float64, device=c.device)
     rc = lib().skew_eigvals(c.h, n, _dp(Ac.data_ptr()), Ac.stride(1), nev, _dp(lam.data_ptr()))

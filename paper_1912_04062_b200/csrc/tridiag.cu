@@ -693,8 +693,10 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
   w.lamv = ar.take<double>(ne);
   w.gblk = ar.take<double>(ne);
   w.vblk = ar.take<int64_t>(2 * ne);
-  // bound the interleaved LU workspace to ~1 GiB
-  int64_t batch = std::max<int64_t>(1, std::min<int64_t>(ne, (int64_t)(16ll << 30) / (49 * nn)));
+  // bound the interleaved LU workspace: 16 GiB up to n = 40000, 4 GiB beyond (n = 65536 with
+  // vectors on 4 GPUs must fit next to A, the reflector stores and X in 178 GiB)
+  const int64_t lu_cap = (nn > 40000) ? (4ll << 30) : (16ll << 30);
+  int64_t batch = std::max<int64_t>(1, std::min<int64_t>(ne, lu_cap / (49 * nn)));
   w.batch = batch;
   w.inv = ar.take<double>((size_t)5 * nn * batch + batch);
   w.inv_in = ar.take<unsigned char>((size_t)nn * batch);
