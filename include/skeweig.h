@@ -64,6 +64,7 @@ extern "C" {
 #define SKEW_WS_HOST_STAGING 2     /* room to stage host A (n x n) */
 #define SKEW_WS_BSE 4              /* room for the BSE front-end (Cholesky factor) */
 #define SKEW_WS_BSE_BACKTRANSFORM 8 /* room for skew_bse_backtransform's scratch (16 n2 nev bytes) */
+#define SKEW_WS_ONESTEP 16         /* size for skew_eig_onestep (with SKEW_WS_VECTORS for vectors) */
 
 /* skew_eig_bse flags */
 #define SKEW_BSE_HAMILTONIAN_Y 1   /* return y = J L z (H y = -i lambda y, H = -J M) instead of z */
@@ -145,6 +146,18 @@ int skew_eigvals(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, d
  * nev 5, flags 6, lambda 7, Zre 8, Zim 9, ldz 10. */
 int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, int flags,
                  double* lambda, double* Zre, double* Zim, int64_t ldz, int64_t* pivot_out);
+
+/* One-step route (the paper's ELPA1-style GPU variant, PAPER.md:359-404,
+ * Eqs. (2)-(5), Fig. 4): A reduced directly to tridiagonal form, one Householder
+ * reflector per column, blocked by 64 columns (a skew matrix-vector product over the
+ * trailing matrix per column, a skew rank-128 update per panel); then the same tridiagonal
+ * solve and D assembly, and ONE back-transformation with the n-2 reflectors (merged compact
+ * WY, the BT1 kernels).  Same result as skew_eig (eigenvalues to rounding; eigenvectors up
+ * to phase).  DEVICE arrays only; Zre = Zim = NULL for eigenvalues only.  Workspace: size
+ * with skew_workspace_size(ctx, n, nev, SKEW_WS_ONESTEP | SKEW_WS_VECTORS, ...).  Arguments
+ * and status codes as skew_eig (host pointers: -i). */
+int skew_eig_onestep(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev,
+                     double* lambda, double* Zre, double* Zim, int64_t ldz);
 
 /* Full BSE H_BS pipeline, step 1 (Eq. (10)):
  * M = [[Re(A+B), Im(A-B)], [-Im(A+B), Re(A-B)]] for H_BS = [[A, B], [-B-bar, -A-bar]]

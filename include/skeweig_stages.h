@@ -42,7 +42,7 @@ int skew_stage_tridiag_eig(skew_ctx ctx, int64_t n, const double* alpha, int64_t
  * returns, for the last call, the number of launches per class and -- when
  * profiling is on -- the summed device time (ms) of each class measured with CUDA
  * events recorded on the context stream around the launches. */
-#define SKEW_KERNEL_CLASSES 18
+#define SKEW_KERNEL_CLASSES 20
 int skew_set_profiling(skew_ctx ctx, int on);
 int skew_kernel_stats(skew_ctx ctx, double* ms_out, int64_t* launches_out, int count);
 const char* skew_kernel_class_name(int cls);

@@ -16,7 +16,7 @@ column-major layout the C-ABI takes).
 import ctypes
 import os
 
-__all__ = ["lib", "Context", "VirtualGroup", "skew_eig", "skew_eig_range", "skew_eig_host_range", "skew_eigvals", "skew_eig_bse", "bse_hbs_eig", "skew_eig_host",
+__all__ = ["lib", "Context", "VirtualGroup", "skew_eig", "skew_eig_range", "skew_eig_host_range", "skew_eigvals", "skew_eig_onestep", "skew_eig_bse", "bse_hbs_eig", "skew_eig_host",
            "reduce_to_band", "band_to_tridiag", "tridiag_eig", "expand_half_spectrum", "SkewError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -28,6 +28,7 @@ SKEW_WS_HOST_STAGING = 2
 SKEW_WS_BSE = 4
 SKEW_WS_BSE_BACKTRANSFORM = 8
 SKEW_BSE_HAMILTONIAN_Y = 1
+SKEW_WS_ONESTEP = 16
 SKEW_ERR_NOCONV = 1
 SKEW_ERR_NOT_DEFINITE = 4
 
@@ -50,6 +51,7 @@ EXPORTS = {
     "skew_set_workspace": ([_vp, _vp, ctypes.c_size_t], ctypes.c_int),
     "skew_eig": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
     "skew_eigvals": ([_vp, _i64, _dp, _i64, _i64, _dp], ctypes.c_int),
+    "skew_eig_onestep": ([_vp, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
     "skew_eig_range": ([_vp, _i64, _dp, _i64, _i64, _i64, _i64, _dp, _dp, _dp, _i64], ctypes.c_int),
     "skew_eig_bse": ([_vp, _i64, _dp, _i64, _i64, ctypes.c_int, _dp, _dp, _dp, _i64, ctypes.POINTER(_i64)],
                      ctypes.c_int),
@@ -66,7 +68,7 @@ EXPORTS = {
     "skew_kernel_stats": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), ctypes.c_int], ctypes.c_int),
     "skew_kernel_class_name": ([ctypes.c_int], ctypes.c_char_p),
 }
-KERNEL_CLASSES = 18
+KERNEL_CLASSES = 20
 
 STAGES = ["f2b", "b2t", "tridiag", "bt2", "bt1", "output", "bse"]
 
@@ -295,6 +297,28 @@ def skew_eigvals(A, nev=None, ctx=None, overwrite_a=False):
     lam = torch.empty(max(nev, 1), dtype=torch.float64, device=c.device)
     rc = lib().skew_eigvals(c.h, n, _dp(Ac.data_ptr()), Ac.stride(1), nev, _dp(lam.data_ptr()))
     c._check(rc, allow=(SKEW_ERR_NOCONV,))
+    return lam[:nev]
+
+
+def skew_eig_onestep(A, nev=None, ctx=None, want_vectors=True, overwrite_a=False):
+    """The one-step route: A -> tridiagonal directly
+    (one reflector per column), same tridiagonal solve, one back-transformation.  Returns
+    (lam, Zre, Zim) like skew_eig, or lam when want_vectors is False."""
+    torch = _torch()
+    c = _ctx(ctx)
+    n = A.shape[0]
+    nev = n // 2 if nev is None else nev
+    Ac = A if (overwrite_a and A.stride(0) == 1) else _colmajor(torch, A.to(device=c.device, dtype=torch.float64))
+    c.ensure_workspace(n, nev, SKEW_WS_ONESTEP | (SKEW_WS_VECTORS if want_vectors else 0))
+    lam = torch.empty(max(nev, 1), dtype=torch.float64, device=c.device)
+    Zre = _new_colmajor(torch, n, max(nev, 1), c.device) if want_vectors else None
+    Zim = _new_colmajor(torch, n, max(nev, 1), c.device) if want_vectors else None
+    rc = lib().skew_eig_onestep(c.h, n, _dp(Ac.data_ptr()), Ac.stride(1), nev, _dp(lam.data_ptr()),
+                                _dp(Zre.data_ptr()) if want_vectors else None,
+                                _dp(Zim.data_ptr()) if want_vectors else None, n)
+    c._check(rc, allow=(SKEW_ERR_NOCONV,))
+    if want_vectors:
+        return lam[:nev], Zre[:, :nev], Zim[:, :nev]
     return lam[:nev]
 
 

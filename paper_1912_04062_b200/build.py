@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["api.cu", "f2b.cu", "b2t.cu", "tridiag.cu", "bt1.cu", "bse.cu", "coll.cu"]
+SOURCES = ["api.cu", "f2b.cu", "b2t.cu", "tridiag.cu", "bt1.cu", "bse.cu", "coll.cu", "onestep.cu"]
 HEADERS = ["common.cuh", "gemm_dmma.cuh", "tma_gemm.cuh", "internal.h"]
 
 

@@ -68,6 +68,39 @@ static void plan_layout(Ctx& c, Plan& p, Arena& ar, int64_t n, int64_t nev, int 
   p.scratch = ar.take<double>(64);
 }
 
+// one-step route (NEXT-4): its own layout (reflector store with r0(j) = j*b + 1, no band /
+// bulge-chasing buffers)
+struct PlanOS {
+  F2BLayout L;
+  int64_t n = 0, nev = 0, ldn = 0;
+  double* vstore = nullptr;
+  OneStepWork ow;
+  double* alpha = nullptr;
+  double* lam = nullptr;
+  TridWork tw;
+  double* Q = nullptr;
+  double* X = nullptr;
+  BT1Work b1;
+  int64_t* status = nullptr;
+};
+
+static void plan_onestep(Ctx& c, PlanOS& p, Arena& ar, int64_t n, int64_t nev, bool vec) {
+  p.n = n; p.nev = nev;
+  p.ldn = (n + 1) & ~int64_t(1);
+  p.L.init(n, c.prm.b, c.prm.bt1_merge, true);
+  if (vec) p.vstore = ar.take<double>((size_t)std::max<int64_t>(p.L.vstore_elems, 1));
+  onestep_reserve(ar, p.L, p.ow);
+  p.alpha = ar.take<double>(std::max<int64_t>(n, 1));
+  p.lam = ar.take<double>(std::max<int64_t>(nev, 1));
+  trid_reserve(ar, n, nev, vec, p.tw, c.prm.reorth_w);
+  if (vec) {
+    p.Q = ar.take<double>((size_t)p.ldn * std::max<int64_t>(nev, 1));
+    p.X = ar.take<double>((size_t)p.ldn * 2 * std::max<int64_t>(nev, 1));
+    bt1_reserve(ar, p.L, 2 * nev, p.b1);
+  }
+  p.status = ar.take<int64_t>(4);
+}
+
 static bool plan_bind(Ctx& c, Plan& p, int64_t n, int64_t nev, int flags) {
   Arena ar;
   ar.base = (char*)c.ws;
@@ -135,7 +168,8 @@ static void kcollect(skew_ctx ctx) {
 }
 static const char* kNames[KC_COUNT] = {"panel_qr", "vt", "skew_symm", "w_correction", "skew_r2k", "band_extract",
                                        "bulge_chase", "bisection", "inverse_iteration", "reorth", "assemble_D",
-                                       "bt2_tbuild", "bt2_apply", "bt1_prep", "bt1_z", "bt1_update", "output", "bse"};
+                                       "bt2_tbuild", "bt2_apply", "bt1_prep", "bt1_z", "bt1_update", "output", "bse",
+                                       "onestep_skew_mv", "onestep_column"};
 
 extern "C" {
 
@@ -269,10 +303,15 @@ int skew_workspace_size(skew_ctx ctx, int64_t n, int64_t nev, int flags, size_t*
   if (n < 1) return -2;
   if (nev < 0 || nev > n / 2) return -3;
   if (!bytes) return -5;
-  Plan p;
   Arena ar;
   ar.measuring = true;
-  plan_layout(ctx->c, p, ar, n, nev, flags);
+  if (flags & SKEW_WS_ONESTEP) {
+    PlanOS po;
+    plan_onestep(ctx->c, po, ar, n, nev, (flags & SKEW_WS_VECTORS) != 0);
+  } else {
+    Plan p;
+    plan_layout(ctx->c, p, ar, n, nev, flags);
+  }
   *bytes = ar.off + 4096;
   return SKEW_OK;
 }
@@ -564,6 +603,77 @@ int skew_eig_bse(skew_ctx ctx, int64_t n, double* M, int64_t ldm, int64_t nev, i
     CK(cudaStreamSynchronize(st), "sync");
   }
   return rc;
+}
+
+// ------------------------------------------------------------------------------------
+// NEXT-4: one-step route (onestep.cu), device arrays only
+int skew_eig_onestep(skew_ctx ctx, int64_t n, double* A, int64_t lda, int64_t nev, double* lambda, double* Zre,
+                     double* Zim, int64_t ldz) {
+  if (!ctx) return -1;
+  if (n < 1) return -2;
+  if (!A || !is_device_ptr(A)) return -3;
+  if (lda < n) return -4;
+  if (nev < 1 || nev > n / 2) return -5;
+  if (!lambda || !is_device_ptr(lambda)) return -6;
+  if (!Zre && Zim) return -7;
+  const bool vec = (Zre != nullptr);
+  if (vec && (!is_device_ptr(Zre))) return -7;
+  if (vec && (!Zim || !is_device_ptr(Zim))) return -8;
+  if (vec && ldz < n) return -9;
+  CK(cudaSetDevice(ctx->c.device), "set device");
+  treset(ctx);
+  Ctx& c = ctx->c;
+  cudaStream_t st = c.stream;
+  PlanOS p;
+  {
+    Arena ar;
+    ar.base = (char*)c.ws;
+    ar.size = c.ws_bytes;
+    plan_onestep(c, p, ar, n, nev, vec);
+    if (!c.ws || ar.fail) {
+      c.last_error = "workspace missing or too small (size it with SKEW_WS_ONESTEP)";
+      return SKEW_ERR_WORKSPACE;
+    }
+  }
+  {
+    int* flag = reinterpret_cast<int*>(p.status + 2);
+    int h = 0;
+    CK(nonfinite_lower(A, lda, n, false, flag, st), "finite check");
+    CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "finite flag");
+    CK(cudaStreamSynchronize(st), "sync");
+    if (h) return -3;
+  }
+  if (vec && p.L.npanel > 0) CK(bt1_upload_meta(p.L, p.b1, st), "bt1 meta");
+  tstart(ctx, ST_F2B);   // the one-step full -> tridiagonal reduction
+  if (vec) CK(cudaMemsetAsync(p.vstore, 0, sizeof(double) * std::max<int64_t>(p.L.vstore_elems, 1), st), "vstore");
+  if (n >= 2) CK(onestep_run(p.L, A, lda, vec ? p.vstore : nullptr, p.ow, p.alpha, c.num_sms, st), "onestep");
+  tstop(ctx, ST_F2B);
+  tstart(ctx, ST_TRID);
+  int64_t nfail = 0, vlo = 0;
+  CK(trid_run(n, p.alpha, nev, p.lam, vec ? p.Q : nullptr, p.ldn, p.tw, c.prm, &nfail, st, 0, nev, &vlo, nullptr),
+     "tridiagonal");
+  c.last_nfail = nfail;
+  if (vec) {
+    CK(assemble_D(p.Q, p.ldn, n, nev, p.X, p.ldn, st), "assemble D");
+    if (p.ldn > n) CK(cudaMemset2DAsync(p.X + n, p.ldn * 8, 0, (p.ldn - n) * 8, 2 * nev, st), "pad row");
+  }
+  tstop(ctx, ST_TRID);
+  if (vec) {
+    tstart(ctx, ST_BT1);
+    if (p.L.npanel > 0) {
+      CK(onestep_bt_prep(p.L, p.vstore, p.ow.tau, p.b1, st), "onestep bt prep");
+      CK(bt1_apply(p.L, p.vstore, p.ow.tau, nullptr, p.X, p.ldn, 2 * nev, p.b1, st), "onestep bt");
+    }
+    tstop(ctx, ST_BT1);
+  }
+  tstart(ctx, ST_OUT);
+  CK(cudaMemcpyAsync(lambda, p.lam, sizeof(double) * nev, cudaMemcpyDeviceToDevice, st), "lambda out");
+  if (vec) CK(split_output(p.X, p.ldn, n, nev, Zre, Zim, ldz, st), "split output");
+  tstop(ctx, ST_OUT);
+  CK(cudaStreamSynchronize(st), "sync");
+  tcollect(ctx);
+  kcollect(ctx);
+  return nfail > 0 ? SKEW_ERR_NOCONV : SKEW_OK;
 }
 
 // ------------------------------------------------------------------------------------

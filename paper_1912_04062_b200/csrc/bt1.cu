@@ -124,11 +124,20 @@ cudaError_t bt1_upload_meta(const F2BLayout& L, BT1Work& w, cudaStream_t st) {
 // runs it on an auxiliary stream, concurrently with the tridiagonal solve)
 cudaError_t bt1_prep(const F2BLayout& L, const double* vstore, const double* Tpanel, BT1Work& w, cudaStream_t st) {
   if (L.ngroup == 0) return cudaSuccess;
+  cudaError_t e = bt1_gram(L, vstore, w, st);
+  if (e) return e;
+  KScope ks(KC_BT1_PREP, st);
+  bt1_tmerge_kernel<<<(unsigned)L.ngroup, 1024, 0, st>>>(w.G, Tpanel, L.npanel, L.merge, L.b, w.T, w.Y);
+  return cudaGetLastError();
+}
+
+// Gram G_g = V_g^T V_g of every merged group (K x K, DMMA tiles)
+cudaError_t bt1_gram(const F2BLayout& L, const double* vstore, BT1Work& w, cudaStream_t st) {
+  if (L.ngroup == 0) return cudaSuccess;
   const int K = L.merge * L.b;
-  KScope ks(KC_BT1_PREP, st, 2);
+  KScope ks(KC_BT1_PREP, st);
   using TG = GemmTile<64, 64, 16, 32, 32, 2, true, false>;
   bt1_gram_kernel<<<dim3(K / 64, K / 64, (unsigned)L.ngroup), 128, TG::SMEM_BYTES, st>>>(vstore, w.gmeta, K, w.G);
-  bt1_tmerge_kernel<<<(unsigned)L.ngroup, 1024, 0, st>>>(w.G, Tpanel, L.npanel, L.merge, L.b, w.T, w.Y);
   return cudaGetLastError();
 }
 

@@ -24,9 +24,11 @@ namespace cg = cooperative_groups;
 
 namespace sk {
 
-void F2BLayout::init(int64_t n_, int b_, int merge_) {
+void F2BLayout::init(int64_t n_, int b_, int merge_, bool onestep) {
   n = n_; b = b_; merge = merge_;
-  npanel = (n >= 2 + b) ? (n - 2) / b : 0;
+  roff = onestep ? 1 : b;
+  if (onestep) npanel = (n >= 3) ? (n - 2 + b - 1) / b : 0;
+  else npanel = (n >= 2 + b) ? (n - 2) / b : 0;
   ngroup = (npanel + merge - 1) / merge;
   goff.assign(ngroup, 0);
   gld.assign(ngroup, 0);

@@ -70,8 +70,12 @@ struct F2BLayout {
   std::vector<int64_t> goff;   // element offset of group g in the V store
   std::vector<int64_t> gld;    // leading dimension of group g (even)
   int64_t vstore_elems = 0;
-  int64_t r0(int64_t j) const { return (j + 1) * (int64_t)b; }
-  void init(int64_t n_, int b_, int merge_);
+  int64_t roff = 0;            // r0(j) = j*b + roff: b for full->band (V_j below the band),
+                               // 1 for the one-step route (reflector of column c starts at row c+1)
+  int64_t r0(int64_t j) const { return j * (int64_t)b + roff; }
+  // onestep = false: panels j = 0 .. floor((n-2)/b)-1 of the full->band reduction (roff = b);
+  // onestep = true: ceil((n-2)/b) panels of b one-step reflectors (columns 0 .. n-3, roff = 1)
+  void init(int64_t n_, int b_, int merge_, bool onestep = false);
 };
 
 
@@ -81,7 +85,7 @@ struct F2BLayout {
 // launching stream (skew_kernel_stats).
 enum KClass {
   KC_PANEL = 0, KC_VT, KC_SYMM, KC_WCORR, KC_R2K, KC_BAND, KC_CHASE, KC_TRID_BISECT, KC_TRID_INV, KC_TRID_REORTH,
-  KC_ASSEMBLE, KC_BT2_T, KC_BT2, KC_BT1_PREP, KC_BT1_Z, KC_BT1_UPD, KC_OUT, KC_BSE, KC_COUNT
+  KC_ASSEMBLE, KC_BT2_T, KC_BT2, KC_BT1_PREP, KC_BT1_Z, KC_BT1_UPD, KC_OUT, KC_BSE, KC_OS_MV, KC_OS_COL, KC_COUNT
 };
 struct Prof {
   bool on = false;
@@ -190,6 +194,19 @@ struct BT1Work {
   int64_t* gmeta = nullptr;   // per group: V-store offset, ld, rows
 };
 
+// onestep.cu: the one-step (ELPA1-style) route, SURVEY 8(f) NEXT-4
+struct OneStepWork {
+  int64_t ldp = 0;
+  double* PV = nullptr;     // panel [V | W]  (ldp x 2b)
+  double* QW = nullptr;     // panel [W | -V]
+  double* ypart = nullptr;  // skew mat-vec tile partials
+  double* y = nullptr;
+  double* pq = nullptr;
+  double* npart = nullptr;
+  double* tau = nullptr;    // n (per column)
+  double* sub = nullptr;    // n (beta per column)
+};
+
 // coll.cu: collectives over NCCL or over virtual ranks (P contexts on one device)
 VGroup* vgroup_new(int P);
 void vgroup_free(VGroup* g);
@@ -237,6 +254,13 @@ cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, dou
 void bt1_reserve(Arena& ar, const F2BLayout& L, int64_t ncols, BT1Work& w);
 cudaError_t bt1_upload_meta(const F2BLayout& L, BT1Work& w, cudaStream_t st);
 cudaError_t bt1_prep(const F2BLayout& L, const double* vstore, const double* Tpanel, BT1Work& w, cudaStream_t st);
+cudaError_t bt1_gram(const F2BLayout& L, const double* vstore, BT1Work& w, cudaStream_t st);
+// onestep.cu
+void onestep_reserve(Arena& ar, const F2BLayout& L, OneStepWork& w);
+cudaError_t onestep_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, OneStepWork& w, double* alpha,
+                        int nsm, cudaStream_t st);
+cudaError_t onestep_bt_prep(const F2BLayout& L, const double* vstore, const double* tau, BT1Work& w,
+                            cudaStream_t st);
 cudaError_t bt1_apply(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,
                       int64_t ldx, int64_t ncols, BT1Work& w, cudaStream_t st);
 cudaError_t bt1_run(const F2BLayout& L, const double* vstore, const double* tau_all, const double* Tpanel, double* X,

@@ -467,3 +467,34 @@ def test_bse_stage_bad_arguments(sk):
     assert L.skew_bse_build_M(c.h, 4, A.data_ptr(), 4, A.data_ptr(), 4, M.data_ptr(), 7) == -8
     assert L.skew_bse_backtransform(c.h, 7, M.data_ptr(), 8, 1, M.data_ptr(), M.data_ptr(), 8,
                                     A.data_ptr(), 8) == -2
+
+
+# ------------------------------------------------------------------ NEXT-4: one-step route
+@pytest.mark.parametrize("n", [2, 3, 4, 65, 66, 129, 130, 257, 600, 1090])
+def test_onestep_vs_oracle(sk, n):
+    """skew_eig_onestep: the same Householder sequence
+    as the oracle's one-step O2, blocked by 64 columns on the GPU; eigenpairs against the
+    oracle (eigenvalues, residual, orthogonality, subspace)."""
+    A = skewgen.random_skew(n, 7000 + n)
+    lam_o, Zre_o, Zim_o, st = oracle.skew_eig(A)
+    assert st == 0
+    lam, Zre, Zim = sk.skew_eig_onestep(_cuda(A))
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
+
+
+def test_onestep_partial_eigvals_and_structured(sk):
+    n = 300
+    A = skewgen.random_skew(n, 99)
+    lam_o = oracle.skew_eig(A, want_vectors=False)[0]
+    lam = sk.skew_eig_onestep(_cuda(A), want_vectors=False).cpu().numpy()
+    assert np.max(np.abs(lam - lam_o)) <= 1e-12 * np.linalg.norm(A)
+    lam, Zre, Zim = sk.skew_eig_onestep(_cuda(A), 37)
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o[:37])
+    J = skewgen.J_matrix(128)
+    lam, Zre, Zim = sk.skew_eig_onestep(_cuda(J))
+    _check_pairs(J, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), np.ones(64))
+    T = skewgen.skew_toeplitz(200)
+    k = np.arange(1, 101)
+    lam_t = 2 * np.cos(k * np.pi / 201)
+    lam, Zre, Zim = sk.skew_eig_onestep(_cuda(T))
+    _check_pairs(T, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_t)
