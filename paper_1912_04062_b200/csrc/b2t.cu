@@ -733,10 +733,6 @@ __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_
   const int cx = 8 * warp;   // this warp's columns cx .. cx+7 of the strip
   int64_t blk = blk0, t = 0;
   int off = 0;
-  if (gskew > 0 && (warp & 1)) {   // experiment: odd warps start gskew cycles late
-    const long long t0 = clock64();
-    while (clock64() - t0 < gskew) { }
-  }
   for (int64_t q = 0;; q++) {
     if (prof) { tprev = clock64(); nsteps++; }
     // The [U | -V] block and the window rows have separate barriers: inside a sweep block the
@@ -836,27 +832,14 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
       a.AB = w.AB; a.ldab = L.ldab; a.n = n; a.b = L.b; a.k2 = L.k2; a.progress = w.progress;
       a.qv = w.qv; a.qtau = w.qtau; a.gofs = w.gofs;
       a.dbg = nullptr;
-      if (getenv("SKEWEIG_CHASE_DBG")) {   // debug instrumentation only
-        cudaError_t me = cudaMalloc(&a.dbg, 48 * sizeof(long long));
-        if (me) { fprintf(stderr, "[chase dbg] cudaMalloc failed: %s\n", cudaGetErrorString(me)); a.dbg = nullptr; }
-        else cudaMemsetAsync(a.dbg, 0, 48 * sizeof(long long), st);
-      }
       int G = chase_grid(n, L.b, nsm, 2);
       if (const char* gg = getenv("SKEWEIG_CHASE_G")) G = std::max(1, std::min(G, atoi(gg)));   // experiments
       size_t smem = (size_t)(2 * L.b + 1) * (2 * L.b + 2) * sizeof(double);
       void* args[] = {&a};
-      e = cudaFuncSetAttribute(chase_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = set_smem_attr((const void*)chase_kernel<64>, (int)smem);
       if (e) return e;
       e = cudaLaunchCooperativeKernel((void*)chase_kernel<64>, dim3(G), dim3(kChaseThreads), args, smem, st);
       if (e) return e;
-      if (a.dbg) {
-        long long h[48];
-        cudaMemcpyAsync(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
-        fprintf(stderr, "[chase dbg] G=%d tasks(cta0)=%lld  per task: wait %.0f work %.0f (load %.0f products %.0f "
-                "update %.0f end %.0f) cycles\n", G, h[2], (double)h[0] / h[2], (double)h[1] / h[2],
-                (double)h[3] / h[2], (double)h[4] / h[2], (double)h[5] / h[2], (double)h[6] / h[2]);
-        cudaFree(a.dbg);
-      }
     }
     alpha_from_band_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.AB, L.ldab, n, alpha);
   }
@@ -864,7 +847,7 @@ cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cuda
 }
 
 // per-strip time of a 96- / 32-wide strip relative to a 64-wide one (tools/bt2_time.py)
-static constexpr double kNB96Cost = 1.5, kNB32Cost = 0.55;
+static constexpr double kNB96Cost = 1.47, kNB32Cost = 0.64;
 
 // ring of RW + BB rows: within a sweep block step q+1's new rows reuse step q-1's leaving
 // rows; at a block boundary the producer writes the last window back before loading the
@@ -893,8 +876,7 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
   cudaError_t e;
   constexpr int K2 = kBT2K2, RW = kBT2RW, RING = kBT2Ring, BB = kBT2BB;
   if (L.k2 != K2 || L.b != BB) return cudaErrorInvalidValue;
-  long long* dbgp = nullptr;
-  if (getenv("SKEWEIG_BT2_DBG")) cudaMalloc(&dbgp, 6 * sizeof(long long));   // debug instrumentation only
+  long long* dbgp = nullptr;   // per-step cycle counters of CTA 0 (instrumentation hook, unused)
   // Column strips: 64 wide (best DMMA / smem ratio) and 32 wide (~0.55x the time of a
   // 64-wide strip, measured: tools/bt2_time.py).  Every strip runs the whole step sequence,
   // so the kernel time is (#waves) x (strip time); pick the mix of n64 wide and n32 narrow
@@ -935,8 +917,7 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
   const int64_t c96 = std::min<int64_t>(ncols, 96 * n96);
   const int64_t c64 = std::min<int64_t>(ncols - c96, 64 * n64);
   const int64_t c32 = ncols - c96 - c64;
-  int gskew = 0;
-  if (const char* v = getenv("SKEWEIG_BT2_SKEW")) gskew = atoi(v);   // experiments
+  const int gskew = 0;
   auto launch = [&](auto kern, size_t smem, int NBv, int64_t cbeg, int64_t cnt, int ns) -> cudaError_t {
     if (cnt <= 0) return cudaSuccess;
     cudaError_t e2 = set_smem_attr((const void*)kern, (int)smem);
@@ -960,14 +941,6 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
   if (e) return e;
   e = launch(bt2_ws_kernel<32, K2, RW, RING, BB, false>, BT2Cfg<32, K2, RW, RING, BB>::SMEM, 32, c96 + c64, c32, 1);
   if (e) return e;
-  if (dbgp) {
-    long long h[6];
-    cudaMemcpyAsync(h, dbgp, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    fprintf(stderr, "[bt2 dbg] steps %lld  per-step cycles (warp 0): wait %.0f gemm1 %.0f gemm2 %.0f\n", h[5],
-            (double)h[0] / h[5], (double)h[1] / h[5], (double)h[2] / h[5]);
-    cudaFree(dbgp);
-  }
   return cudaGetLastError();
 }
 

@@ -1149,11 +1149,7 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
     ca.p.R = Rc;
     ca.p.smem_rows = (int)Rc;
     ca.scr = w.cqr;
-    static long long* dbgp = nullptr;
-    if (getenv("SKEWEIG_PANEL_DBG") && j == 3) {
-      if (!dbgp) cudaMalloc(&dbgp, 32 * sizeof(long long));
-      ca.dbg = dbgp;
-    }
+    ca.dbg = nullptr;
     void* cargs[] = {&ca};
     // smem: the CholQR layout, or the Householder fallback's (same grid, Rc rows per CTA)
     const size_t sm_c = std::max(cqr_smem, std::max((size_t)b * Rc * sizeof(double), tbuild) + extra);
@@ -1161,16 +1157,6 @@ cudaError_t f2b_panel(const F2BLayout& L, int64_t j, double* A, int64_t lda, dou
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, panel_cqr_kernel<64>, 256, sm_c);
     if (occ * nsm >= Gc) {
       e = cudaLaunchCooperativeKernel((void*)panel_cqr_kernel<64>, dim3(Gc), dim3(256), cargs, sm_c, st);
-      if (ca.dbg) {
-        long long h[32];
-        cudaMemcpyAsync(h, ca.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        for (int c = 0; c < 2; c++) {
-          fprintf(stderr, "[cqr cta%d]", c);
-          for (int i = 1; i < 16 && h[c * 16 + i] > h[c * 16]; i++) fprintf(stderr, " %lld", h[c * 16 + i] - h[c * 16 + i - 1]);
-          fprintf(stderr, "\n");
-        }
-      }
       return e;
     }
   }

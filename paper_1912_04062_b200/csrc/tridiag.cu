@@ -908,20 +908,11 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
         ra.gbar = w.gbar;
         e = cudaMemsetAsync(w.gbar, 0, sizeof(unsigned), st);
         if (e) return e;
-        static long long* dbgp = nullptr;
-        if (getenv("SKEWEIG_REORTH_DBG") && !dbgp) cudaMalloc(&dbgp, 8 * sizeof(long long));   // debug only
-        ra.dbg = getenv("SKEWEIG_REORTH_DBG") ? dbgp : nullptr;
+        ra.dbg = nullptr;
         void* args[] = {&ra};
         KScope ks(KC_TRID_REORTH, st);
         e = cudaLaunchCooperativeKernel((void*)td_reorth_fused_kernel, dim3(G), dim3(256), args, smem, st);
         if (e) return e;
-        if (ra.dbg) {
-          long long h[8];
-          cudaMemcpyAsync(h, ra.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
-          cudaStreamSynchronize(st);
-          fprintf(stderr, "[reorth dbg] G=%d R=%d nblk=%d cycles: misc %lld gram %lld sync %lld reduce %lld rowmul %lld "
-                  "chol %lld writeback %lld\n", G, R, nblk, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
-        }
         // the host copy of blk must outlive the async copy
         e = cudaStreamSynchronize(st);
         if (e) return e;

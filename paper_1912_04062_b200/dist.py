@@ -1,14 +1,21 @@
 """Multi-GPU layer (one process per GPU, torch.distributed for the plumbing).
 
-Round-1 partition: the eigenpairs are split into contiguous index
-ranges [k0, k1) per rank.  Every rank runs the reduction stages (full->band, bulge chasing,
-bisection) on the same input -- they are deterministic, so every rank obtains bit-identical
-reflectors and eigenvalues -- and then computes only its own eigenvectors: inverse
-iteration, D assembly, BT2 and BT1 on its 2*(k1-k0) columns of [Re | Im].  The
-back-transformations of different column blocks are independent (PAPER.md:336-338:
-"applied on the real and imaginary part independently"), so the sharded part needs no
-data-path collective.  Gathering the vectors (optional, for callers that want them on one
-rank) is a plain all_gather.
+Partition:
+- full->band is distributed inside the library over a collective context
+  (skew_ctx_create_dist): 1D block-cyclic 64-wide column blocks (owner of block q = q mod P),
+  the owner factors each panel and NCCL-broadcasts V / T / tau, every rank forms its partial
+  skew-SYMM product from its own column blocks, the partials are summed with an allreduce,
+  W is formed redundantly and each rank applies the rank-2k update to its own column blocks;
+- the band is combined with one allreduce and the bulge chase runs replicated (deterministic,
+  bit-identical on every rank);
+- the multisection eigenvalue search is sharded by task slice plus an allgather;
+- the eigenpairs are split into contiguous index ranges [k0, k1) per rank: inverse
+  iteration (with ghost vectors for the re-orthogonalisation window), D assembly, BT2 and BT1
+  on the rank's 2*(k1-k0) columns of [Re | Im], with no data-path collective (PAPER.md:336-338:
+  "applied on the real and imaginary part independently").
+Gathering the vectors (optional, for callers that want them on one rank) is a plain
+all_gather.  The same distributed code runs on one GPU through virtual ranks
+(Context(virtual=...), tests/test_gpu_virtual_ranks.py).
 """
 import os
 
