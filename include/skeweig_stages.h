@@ -49,9 +49,11 @@ const char* skew_kernel_class_name(int cls);
 
 /* The rank-2k update's lower-triangular tile schedule (host function, no GPU needed):
  * fills tm_out / tn_out (capacity cap) with the (row tile, column tile) pairs the
- * skew rank-2k kernel of rank `rank` of `nranks` visits on a trailing matrix of ntm x ntm
- * tiles (64 x 64 tiles, 1D block-cyclic column ownership rank(q) = (q - qoff) mod nranks
- * with qoff = 0 here), in launch order.  Returns the count (or -i for a bad argument i).
+ * skew rank-2k kernel of rank `rank` of `nranks` visits on a trailing matrix of order
+ * ntm*128 (128-row x 64-column tiles of the TMA-fed kernel; 1D block-cyclic ownership of the
+ * 64-wide column blocks, rank(q) = (q - qoff) mod nranks with qoff = 0 here), in launch order:
+ * tile (tm, tn) covers rows [128 tm, 128 tm + 128) and columns [64 tn, 64 tn + 64) and is
+ * visited iff it meets the strictly lower triangle.  Returns the count (or -i for argument i).
  * Tests check that the ranks' sets partition the lower triangle (tests/test_tile_schedule.py). */
 int64_t skew_tile_schedule(int64_t ntm, int nranks, int rank, int64_t* tm_out, int64_t* tn_out, int64_t cap);
 

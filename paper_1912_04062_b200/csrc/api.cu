@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "gemm_dmma.cuh"
+#include "tma_gemm.cuh"
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
@@ -236,24 +237,24 @@ int64_t skew_tile_schedule(int64_t ntm, int nranks, int rank, int64_t* tm_out, i
   if (nranks < 1) return -2;
   if (rank < 0 || rank >= nranks) return -3;
   if (cap < 0 || ((!tm_out || !tn_out) && cap > 0)) return -6;
-  // the same grid size and tile decoding as gemm_dmma<..., TRI> (gemm_dmma.cuh)
-  int64_t cnt;
+  // the rank-2k kernel's schedule (tma_gemm<128, 64, ..., TRI>): 128-row x 64-column tiles of
+  // an ntm*128 square trailing matrix, the same host/device tile decoder as the kernel
+  const int64_t tmr = ntm, tn = 2 * ntm;
+  TmaGemmArgs g;
+  g.ntiles = tmr * (tmr + 1);   // R = 2: sum_tm 2 (tm + 1)
   if (nranks > 1) {
-    const int64_t off = rank, st = nranks;
-    if (off >= ntm) return 0;
-    const int64_t kmax = (ntm - off + st - 1) / st;
-    cnt = kmax * (ntm - off) - st * kmax * (kmax - 1) / 2;
-  } else {
-    cnt = ntm * (ntm + 1) / 2;
+    if (rank >= tn) return 0;
+    g.col_stride = nranks; g.col_off = rank; g.ntm = tmr;
+    g.kloc = (tn - rank + nranks - 1) / nranks;
+    g.ntiles = tri_strided_count(g.kloc, tmr, rank, nranks, 2);
   }
-  for (int64_t t = 0; t < cnt && t < cap; t++) {
-    int64_t tm, tn;
-    if (nranks > 1) tri_tile_strided(t, ntm, nranks, rank, tm, tn);
-    else tri_tile(t, 1, tm, tn);
-    tm_out[t] = tm;
-    tn_out[t] = tn;
+  for (int64_t t = 0; t < g.ntiles && t < cap; t++) {
+    int64_t a, b;
+    tma_tile_coords<128, 64>(g, t, true, a, b);
+    tm_out[t] = a;
+    tn_out[t] = b;
   }
-  return cnt;
+  return g.ntiles;
 }
 
 int skew_vgroup_create(int nranks, void** out) {

@@ -35,7 +35,26 @@ struct TmaGemmArgs {
   int64_t tri_off = 1;   // TRI: write (m, n) iff m - n >= tri_off
   int64_t ntiles = 0;    // tile count (TRI: lower-triangular tile set)
   int64_t tn_count = 0;  // non-TRI: number of column tiles
+  // TRI, distributed (col_stride > 1): only the column tiles tn = col_off + col_stride * i
+  // (BN wide, the rank's 1D block-cyclic columns); ntm = row tiles (BM high)
+  int col_stride = 1, col_off = 0;
+  int64_t ntm = 0, kloc = 0;   // kloc = number of local column tiles
 };
+
+// sum_{i<k} floor((off + s i) / R), R in {1, 2}
+__host__ __device__ inline int64_t tri_floor_sum(int64_t k, int64_t off, int64_t s, int R) {
+  const int64_t lin = k * off + s * k * (k - 1) / 2;
+  if (R == 1) return lin;
+  int64_t odd;
+  if ((s & 1) == 0) odd = k * (off & 1);
+  else odd = (off & 1) ? (k + 1) / 2 : k / 2;
+  return (lin - odd) / 2;
+}
+// number of (row tile, column tile) pairs of the strided lower-triangular tile set among the
+// first k local column tiles: S(k) = sum_{i<k} (ntm - floor(tn_i / R))
+__host__ __device__ inline int64_t tri_strided_count(int64_t k, int64_t ntm, int64_t off, int64_t s, int R) {
+  return k * ntm - tri_floor_sum(k, off, s, R);
+}
 
 // 2-D tiled TMA load of box (c0 = contiguous coordinate, c1 = strided coordinate)
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -65,8 +84,18 @@ struct TmaGemmCfg {
 };
 
 template <int BM, int BN>
-__device__ __forceinline__ void tma_tile_coords(const TmaGemmArgs& g, int64_t t, bool tri, int64_t& tm, int64_t& tn) {
-  if (tri) {
+__host__ __device__ __forceinline__ void tma_tile_coords(const TmaGemmArgs& g, int64_t t, bool tri, int64_t& tm, int64_t& tn) {
+  if (tri && g.col_stride > 1) {
+    constexpr int R = BM / BN;
+    int64_t lo = 0, hi = g.kloc;   // S(lo) <= t < S(hi); S is increasing on [0, kloc]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (tri_strided_count(mid, g.ntm, g.col_off, g.col_stride, R) <= t) lo = mid;
+      else hi = mid;
+    }
+    tn = g.col_off + (int64_t)g.col_stride * lo;
+    tm = tn / R + (t - tri_strided_count(lo, g.ntm, g.col_off, g.col_stride, R));
+  } else if (tri) {
     tri_tile(t, BM / BN, tm, tn);
   } else {
     tm = t / g.tn_count;
@@ -235,7 +264,7 @@ template <int BM, int BN, int BK, int NS, bool A_KMAJ, bool B_NMAJ, bool HAS_C, 
 cudaError_t tma_gemm(const GemmArgs& ga, int nsm, cudaStream_t st) {
   using Cfg = TmaGemmCfg<BM, BN, BK, NS, A_KMAJ, B_NMAJ, HAS_C>;
   if (ga.M <= 0 || ga.N <= 0) return cudaSuccess;
-  if (!tma_gemm_ok(ga) || (TRI && ga.col_stride != 1) || (HAS_C != (ga.beta != 0.0))) return cudaErrorNotSupported;
+  if (!tma_gemm_ok(ga) || (!TRI && ga.col_stride != 1) || (HAS_C != (ga.beta != 0.0))) return cudaErrorNotSupported;
   CUtensorMap mA, mB, mC;
   // A: non-KMAJ = column-major M x K (box BM+4 rows x BK); KMAJ = column-major K x M (box BK+4 x BM)
   bool ok = A_KMAJ ? tma_map_2d(&mA, ga.A, ga.K, ga.M, ga.lda, BK + 4, BM)
@@ -252,6 +281,16 @@ cudaError_t tma_gemm(const GemmArgs& ga, int nsm, cudaStream_t st) {
   const int64_t tm = (ga.M + BM - 1) / BM, tn = (ga.N + BN - 1) / BN;
   g.tn_count = tn;
   g.ntiles = TRI ? (int64_t)(BM / BN) * tm * (tm + 1) / 2 : tm * tn;
+  if (TRI && ga.col_stride > 1) {   // the rank's column tiles only (BN-wide, 1D block-cyclic)
+    g.col_stride = ga.col_stride;
+    g.col_off = ga.col_off;
+    g.ntm = tm;
+    if (ga.col_off >= tn) return cudaSuccess;
+    const int64_t kloc = (tn - ga.col_off + ga.col_stride - 1) / ga.col_stride;
+    g.kloc = kloc;
+    g.ntiles = tri_strided_count(kloc, tm, ga.col_off, ga.col_stride, BM / BN);
+  }
+  if (g.ntiles <= 0) return cudaSuccess;
   auto kern = tma_gemm_kernel<BM, BN, BK, NS, A_KMAJ, B_NMAJ, HAS_C, TRI>;
   cudaError_t e = set_smem_attr((const void*)kern, (int)Cfg::SMEM);
   if (e != cudaSuccess) return e;

@@ -1,8 +1,8 @@
 """CPU checks of the distributed rank-2k tile ownership: the tile
-schedule of the skew rank-2k kernel (skew_tile_schedule, the host copy of the kernel's tile
-decoder tri_tile / tri_tile_strided) visits exactly the lower-triangular 64 x 64 tiles of the
-trailing matrix, and over the ranks of a 1D block-cyclic column distribution the per-rank
-sets partition the lower triangle with rank r owning exactly the column tiles q = r (mod P)."""
+schedule of the skew rank-2k kernel (skew_tile_schedule runs the kernel's own host/device tile
+decoder, tma_tile_coords, for 128-row x 64-column tiles) visits exactly the tiles that meet
+the strictly lower triangle, and over the ranks of a 1D block-cyclic column distribution the
+per-rank sets partition them with rank r owning exactly the column tiles q = r (mod P)."""
 import ctypes
 
 import numpy as np
@@ -30,9 +30,9 @@ def L():
 @pytest.mark.parametrize("ntm", [0, 1, 2, 3, 7, 64, 511, 1023])
 def test_single_device_schedule_is_the_lower_triangle(L, ntm):
     tm, tn = _sched(L, ntm, 1, 0)
-    assert len(tm) == ntm * (ntm + 1) // 2
-    assert np.all(tn <= tm) and np.all(tm < max(ntm, 1))
-    assert len(set(zip(tm.tolist(), tn.tolist()))) == len(tm)
+    want = {(a, b) for a in range(ntm) for b in range(2 * ntm) if 128 * a + 127 > 64 * b}
+    assert len(tm) == len(want) == ntm * (ntm + 1)
+    assert set(zip(tm.tolist(), tn.tolist())) == want
 
 
 @pytest.mark.parametrize("ntm", [1, 2, 5, 8, 9, 64, 255, 512])
@@ -42,8 +42,8 @@ def test_ranks_partition_the_lower_triangle(L, ntm, P):
     for r in range(P):
         tm, tn = _sched(L, ntm, P, r)
         assert np.all(tn % P == r), "rank r owns the column tiles q = r mod P"
-        assert np.all(tn <= tm) and np.all(tm < ntm)
+        assert np.all(128 * tm + 127 > 64 * tn) and np.all(tm < ntm) and np.all(tn < 2 * ntm)
         for a, b in zip(tm.tolist(), tn.tolist()):
             assert (a, b) not in seen, f"tile {(a, b)} visited by ranks {seen[(a, b)]} and {r}"
             seen[(a, b)] = r
-    assert len(seen) == ntm * (ntm + 1) // 2
+    assert len(seen) == ntm * (ntm + 1)
