@@ -109,8 +109,10 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, BK, NS, A_KMAJ, B_NMAJ, HAS
                     const __grid_constant__ CUtensorMap mapC, TmaGemmArgs g) {
   using Cfg = TmaGemmCfg<BM, BN, BK, NS, A_KMAJ, B_NMAJ, HAS_C>;
   using T = typename Cfg::T;
-  extern __shared__ __align__(128) unsigned char sm_raw[];
-  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+  // the dynamic shared memory of a kernel without static shared memory starts at the window's
+  // base (1 KB aligned): no run-time realignment, so the fragment loads stay LDS (a pointer
+  // rebuilt through an integer would turn them into generic loads)
+  extern __shared__ __align__(1024) double sm[];
   double* As = sm;
   double* Bs = As + NS * Cfg::A_ST;
   double* Cs = Bs + NS * Cfg::B_ST;
