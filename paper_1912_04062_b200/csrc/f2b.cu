@@ -1319,7 +1319,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     g0.col_off = 0; g0.col_stride = (int)(ntm + 1);   // tile column 0 only
     {
       KScope ks(KC_R2K, st);
-      e = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 16, 4, false, true, true, true>(g0, nsm, st);
+      e = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 32, 3, false, true, true, true>(g0, nsm, st);
       if (e == cudaErrorNotSupported) e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(g0, st);
     }
     if (e) return e;
@@ -1337,7 +1337,8 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     KScope ks(KC_R2K, st);
     e = cudaErrorNotSupported;
     if (!tma_disabled())   // persistent TMA-fed 128 x 64 tiles (the rank's column tiles when distributed)
-      e = tma_gemm<128, 64, 16, 4, false, true, true, true>(ga, nsm, st);
+      e = tma_gemm<128, 64, 32, 3, false, true, true, true>(ga, nsm, st);   // K = 128: 4 blocks of 32
+
     if (e == cudaErrorNotSupported) e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
   }
   if (e) return e;

@@ -336,7 +336,7 @@ cudaError_t onestep_run(const F2BLayout& L, double* A, int64_t lda, double* vsto
       ga.A = w.PV + nb; ga.lda = w.ldp; ga.B = w.QW + nb; ga.ldb = w.ldp;
       ga.C = A + SK_IDX(c0 + nb, c0 + nb, lda); ga.ldc = lda; ga.alpha = 1.0; ga.beta = 1.0;
       KScope ks(KC_R2K, st);
-      e = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 16, 4, false, true, true, true>(ga, nsm, st);
+      e = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 32, 3, false, true, true, true>(ga, nsm, st);
       if (e == cudaErrorNotSupported) e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
       if (e) return e;
     }

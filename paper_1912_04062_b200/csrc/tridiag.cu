@@ -37,7 +37,34 @@ __device__ __forceinline__ uint64_t td_splitmix64(uint64_t x) {
 // log_2: the Sturm chain (one dependent division per row) is latency-bound, so K-fold more
 // counts per round cost little and the critical path shrinks ~3x for K = 8.  Same stopping
 // rule as plain bisection (reading of PAPER.md:616): width <= max(2 eps max|x|, eps g).
-// Sturm count on block [s0, s0+m): #{eigenvalues < sigma}
+// Sturm count on block [s0, s0+m): #{eigenvalues < sigma} of tridiag(alpha, 0, alpha),
+// q_0 = -sigma, q_k = -sigma - alpha_{k-1}^2 / q_{k-1}, |q_k| < pivmin -> -pivmin.
+// Zero-diagonal aware: two rows per division.  With t = -sigma q_{k-1} - alpha_{k-1}^2,
+// q_k = t / q_{k-1} (its sign is sign(t) * sign(q_{k-1}); |q_k| < pivmin iff |t| < pivmin |q|)
+// and q_{k+1} = -sigma - alpha_k^2 q_{k-1} / t, so the pair costs one division instead of two
+// (the per-row chain is a dependent division, so this halves the latency-bound critical path).
+// Right after a clamped pivot (|q| > 1e150) the two rows are stepped one by one, which keeps
+// sigma * q and alpha^2 * q finite.
+__device__ __forceinline__ void td_sturm_pair(double a, double b, double sigma, double pivmin, double& q, int& cnt) {
+  if (fabs(q) > 1e150) {
+    double qk = -sigma - a / q;
+    if (fabs(qk) < pivmin) qk = -pivmin;
+    cnt += (qk < 0);
+    q = -sigma - b / qk;
+  } else {
+    const double t = fma(-sigma, q, -a);
+    if (fabs(t) < pivmin * fabs(q)) {   // q_k clamped to -pivmin
+      cnt += 1;
+      q = -sigma + b / pivmin;
+    } else {
+      cnt += ((t < 0.0) != (q < 0.0));
+      q = -sigma - (b * q) / t;
+    }
+  }
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += (q < 0);
+}
+
 __device__ __forceinline__ int td_sturm32(const double* __restrict__ a2, int64_t s0, int m, double sigma,
                                           double pivmin) {
   int cnt = 0;
@@ -45,8 +72,8 @@ __device__ __forceinline__ int td_sturm32(const double* __restrict__ a2, int64_t
   if (fabs(q) < pivmin) q = -pivmin;
   cnt += (q < 0);
   const double* p = a2 + s0;
-  // the a2 loads never depend on the chain: issue 16 of them ahead of each 16 steps, so the
-  // step cost is the division chain, not one L2 round trip per row
+  // the a2 loads never depend on the chain: issue 16 of them ahead of each 16 rows, so the
+  // row cost is the division chain, not one L2 round trip per row
   constexpr int U = 16;
   int k = 1;
   for (; k + U <= m; k += U) {
@@ -54,13 +81,10 @@ __device__ __forceinline__ int td_sturm32(const double* __restrict__ a2, int64_t
 #pragma unroll
     for (int u = 0; u < U; u++) av[u] = __ldg(p + k - 1 + u);
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      q = -sigma - av[u] / q;
-      if (fabs(q) < pivmin) q = -pivmin;
-      cnt += (q < 0);
-    }
+    for (int u = 0; u < U; u += 2) td_sturm_pair(av[u], av[u + 1], sigma, pivmin, q, cnt);
   }
-  for (; k < m; k++) {
+  for (; k + 1 < m; k += 2) td_sturm_pair(__ldg(p + k - 1), __ldg(p + k), sigma, pivmin, q, cnt);
+  if (k < m) {
     q = -sigma - __ldg(p + k - 1) / q;
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += (q < 0);
