@@ -557,7 +557,7 @@ template <int NB, int K2, int RW, int RING, int BB, bool SPLIT>
 __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_ws_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols, int64_t n,
                                                        const double* __restrict__ UV, const int64_t* __restrict__ gofs,
                                                        int64_t nblk, long long* dbg, int nsplit_arg,
-                                                       unsigned long long* prog, int gskew) {
+                                                       unsigned long long* prog) {
   using C = BT2Cfg<NB, K2, RW, RING, BB>;
   const int nsplit = SPLIT ? nsplit_arg : 1;   // compile-time 1 on the default path
   extern __shared__ __align__(128) double sh[];
@@ -917,7 +917,6 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
   const int64_t c96 = std::min<int64_t>(ncols, 96 * n96);
   const int64_t c64 = std::min<int64_t>(ncols - c96, 64 * n64);
   const int64_t c32 = ncols - c96 - c64;
-  const int gskew = 0;
   auto launch = [&](auto kern, size_t smem, int NBv, int64_t cbeg, int64_t cnt, int ns) -> cudaError_t {
     if (cnt <= 0) return cudaSuccess;
     cudaError_t e2 = set_smem_attr((const void*)kern, (int)smem);
@@ -929,7 +928,7 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
     }
     KScope ks(KC_BT2, st);
     kern<<<(unsigned)grid, 32 * (NBv / 8 + 4), smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp,
-                                                           ns, w.prog, gskew);
+                                                           ns, w.prog);
     return cudaGetLastError();
   };
   e = launch(bt2_ws_kernel<96, K2, RW, RING, BB, false>, BT2Cfg<96, K2, RW, RING, BB>::SMEM, 96, 0, c96, 1);

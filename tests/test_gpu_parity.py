@@ -498,3 +498,27 @@ def test_onestep_partial_eigvals_and_structured(sk):
     lam_t = 2 * np.cos(k * np.pi / 201)
     lam, Zre, Zim = sk.skew_eig_onestep(_cuda(T))
     _check_pairs(T, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_t)
+
+
+def test_onestep_bad_arguments_and_workspace(sk):
+    L = sk.lib()
+    c = sk.Context()
+    n = 64
+    A = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    lam = torch.zeros(n, dtype=torch.float64, device="cuda")
+    Ah = np.zeros((n, n))
+    # no workspace yet -> SKEW_ERR_WORKSPACE (12) after the argument checks
+    assert L.skew_eig_onestep(c.h, n, A.data_ptr(), n, 16, lam.data_ptr(), None, None, n) == 12
+    c.ensure_workspace(n, 32, sk.SKEW_WS_ONESTEP | sk.SKEW_WS_VECTORS)
+    assert L.skew_eig_onestep(c.h, 0, A.data_ptr(), n, 16, lam.data_ptr(), None, None, n) == -2
+    assert L.skew_eig_onestep(c.h, n, Ah.ctypes.data, n, 16, lam.data_ptr(), None, None, n) == -3
+    assert L.skew_eig_onestep(c.h, n, A.data_ptr(), n - 1, 16, lam.data_ptr(), None, None, n) == -4
+    assert L.skew_eig_onestep(c.h, n, A.data_ptr(), n, 33, lam.data_ptr(), None, None, n) == -5
+    assert L.skew_eig_onestep(c.h, n, A.data_ptr(), n, 16, lam.data_ptr(), None, A.data_ptr(), n) == -7
+    assert L.skew_eig_onestep(c.h, n, A.data_ptr(), n, 16, lam.data_ptr(), A.data_ptr(), None, n) == -8
+    assert L.skew_eig_onestep(c.h, n, A.data_ptr(), n, 16, lam.data_ptr(), A.data_ptr(), A.data_ptr(), n - 1) == -9
+    # the zero matrix: all eigenvalues 0, a valid orthonormal basis
+    lam0, Zre, Zim = sk.skew_eig_onestep(A.clone(), 32, ctx=c)
+    assert torch.all(lam0 == 0).item()
+    Z = Zre.cpu().numpy() + 1j * Zim.cpu().numpy()
+    assert np.max(np.abs(Z.conj().T @ Z - np.eye(32))) <= 1e-12
