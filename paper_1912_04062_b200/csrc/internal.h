@@ -173,6 +173,7 @@ struct TridWork {
   double* lamv = nullptr;      // per-vector perturbed lambda (nev)
   double* gblk = nullptr;      // per-vector block bound
   int64_t* vblk = nullptr;     // 2 * nev (s0, m)
+  unsigned char* single = nullptr;   // per vector: 1 = isolated eigenvalue (twisted factorization)
   double* inv = nullptr;       // inverse iteration work
   unsigned char* inv_in = nullptr;
   int* nfail = nullptr;

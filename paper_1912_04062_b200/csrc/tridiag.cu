@@ -144,6 +144,8 @@ struct InvArgs {
   double* scale;                // [nvec] final 1/||y|| with the dstein sign
   uint64_t seed;
   int* nfail;
+  const unsigned char* single;  // per global vector: 1 = isolated (twisted kernel), 0 = dstein kernel
+  double pivmin;
 };
 
 template <int IU>
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(128) td_inverse_kernel(InvArgs a) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= a.nvec) return;
   const int64_t gv = a.col0 + q;
+  if (a.single[gv]) return;   // isolated eigenvalue: td_twisted_kernel
   const int64_t s0 = a.vs0[gv], m = a.vm[gv];
   const int64_t B = a.nvec;
   double* A_ = a.wa; double* Bb = a.wb; double* C = a.wc; double* D = a.wd; unsigned char* IN = a.win;
@@ -316,11 +319,163 @@ __global__ void __launch_bounds__(128) td_inverse_kernel(InvArgs a) {
 #undef AT
 }
 
+// Isolated eigenvalues (no other eigenvalue within the cluster threshold, reading R9(4)):
+// the eigenvector from ONE twisted factorization of T - lambda I (Fernando / Parlett; the
+// vector step of MRRR, here on the zero-diagonal Lemma-1 tridiagonal) instead of dstein's
+// iterated LU solves.  Two lanes per vector, in parallel: lane h = 0 the forward pivots
+// d_0 = -lambda, d_{k+1} = -lambda - alpha_k^2 / d_k (LDL^T), lane h = 1 the backward pivots
+// delta_{m-1} = -lambda, delta_k = -lambda - alpha_k^2 / delta_{k+1} (UDU^T); twist
+// r = argmin |gamma_k|, gamma_k = d_k + delta_k + lambda (zero diagonal); then z_r = 1,
+// z_k = -(alpha_k / d_k) z_{k+1} (k < r, lane 0) and z_k = -(alpha_{k-1} / delta_k) z_{k-1}
+// (k > r, lane 1).  Pivots below pivmin are replaced by -pivmin (as in the Sturm count).
+// Output as td_inverse_kernel: y [m][nvec] and scale (1/||z||, largest entry positive); the
+// block CGS2 re-orthogonalisation follows unchanged.  Lanes: vector q0 + (lane & 15),
+// role lane >> 4, so both roles walk the interleaved arrays coalesced.
+__global__ void __launch_bounds__(128) td_twisted_kernel(InvArgs a) {
+  const int lane = threadIdx.x & 31, h = lane >> 4;
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32 * 16 + (lane & 15);
+  const bool valid = q < a.nvec;
+  const int64_t gv = a.col0 + (valid ? q : 0);
+  const bool active = valid && a.single[gv];
+  const int64_t s0 = a.vs0[gv], m = active ? a.vm[gv] : 0;
+  const int64_t B = a.nvec;
+#define AT(arr, k) arr[(size_t)(k) * B + q]
+  double* D = a.wa;     // forward pivots d_k
+  double* E = a.wb;     // backward pivots delta_k
+  double* y = a.y;
+  const double lambda = active ? a.lam[gv] : 0.0;
+  const double pivmin = a.pivmin;
+  const double* al = a.alpha + s0;
+  if (active && m == 1) { if (h == 0) { AT(y, 0) = 1.0; a.scale[q] = 1.0; } }
+  const bool work = active && m > 1;
+  // ---- pivots (lane roles in parallel; alpha loads 16 rows ahead of the division chain)
+  if (work) {
+    double piv = -lambda;
+    if (fabs(piv) < pivmin) piv = -pivmin;
+    if (h == 0) {
+      AT(D, 0) = piv;
+      for (int64_t k0 = 0; k0 + 1 < m; k0 += 16) {
+        double av[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) av[u] = (k0 + u + 1 < m) ? al[k0 + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+          const int64_t k = k0 + u;
+          if (k + 1 >= m) break;
+          piv = -lambda - (av[u] * av[u]) / piv;
+          if (fabs(piv) < pivmin) piv = -pivmin;
+          AT(D, k + 1) = piv;
+        }
+      }
+    } else {
+      AT(E, m - 1) = piv;
+      for (int64_t k0 = m - 2; k0 >= 0; k0 -= 16) {
+        double av[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) av[u] = (k0 - u >= 0) ? al[k0 - u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+          const int64_t k = k0 - u;
+          if (k < 0) break;
+          piv = -lambda - (av[u] * av[u]) / piv;
+          if (fabs(piv) < pivmin) piv = -pivmin;
+          AT(E, k) = piv;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // ---- twist index: each role scans half of the rows, then the pair combines
+  double best = INFINITY;
+  int64_t r = 0;
+  if (work) {   // 16 rows of loads in flight ahead of the compares
+    const int64_t k0 = h ? m / 2 : 0, k1 = h ? m : m / 2;
+    for (int64_t kb = k0; kb < k1; kb += 16) {
+      double dv[16], ev[16];
+#pragma unroll
+      for (int u = 0; u < 16; u++)
+        if (kb + u < k1) { dv[u] = AT(D, kb + u); ev[u] = AT(E, kb + u); }
+#pragma unroll
+      for (int u = 0; u < 16; u++)
+        if (kb + u < k1) {
+          const double gk = fabs(dv[u] + ev[u] + lambda);
+          if (gk < best) { best = gk; r = kb + u; }
+        }
+    }
+  }
+  {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, 16);
+    const int64_t orr = __shfl_xor_sync(0xffffffffu, r, 16);
+    if (ob < best || (ob == best && orr < r)) { best = ob; r = orr; }
+  }
+  // ---- z: lane 0 rows r-1 .. 0, lane 1 rows r+1 .. m-1; sum of squares and the largest entry
+  double ssq = 0.0, zmax = 0.0;
+  int64_t jmax = r;
+  if (work) {
+    // the multipliers of a 16-row chunk (loads and divisions off the z chain) first, then
+    // the chunk's products
+    if (h == 0) {
+      double z = 1.0;
+      AT(y, r) = 1.0;
+      ssq = 1.0; zmax = 1.0;
+      for (int64_t kb = r - 1; kb >= 0; kb -= 16) {
+        double mu[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+          const int64_t k = kb - u;
+          mu[u] = (k >= 0) ? -(al[k] / AT(D, k)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+          const int64_t k = kb - u;
+          if (k < 0) break;
+          z = mu[u] * z;
+          AT(y, k) = z;
+          ssq += z * z;
+          if (fabs(z) > zmax) { zmax = fabs(z); jmax = k; }
+        }
+      }
+    } else {
+      double z = 1.0;
+      for (int64_t kb = r + 1; kb < m; kb += 16) {
+        double mu[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+          const int64_t k = kb + u;
+          mu[u] = (k < m) ? -(al[k - 1] / AT(E, k)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+          const int64_t k = kb + u;
+          if (k >= m) break;
+          z = mu[u] * z;
+          AT(y, k) = z;
+          ssq += z * z;
+          if (fabs(z) > zmax) { zmax = fabs(z); jmax = k; }
+        }
+      }
+    }
+  }
+  const double ossq = __shfl_xor_sync(0xffffffffu, ssq, 16);
+  const double ozm = __shfl_xor_sync(0xffffffffu, zmax, 16);
+  const int64_t ojm = __shfl_xor_sync(0xffffffffu, jmax, 16);
+  __syncwarp();
+  if (work && h == 0) {
+    const double tot = ssq + ossq;
+    int64_t jm = jmax;
+    if (ozm > zmax || (ozm == zmax && ojm < jmax)) jm = ojm;
+    double sc = 1.0 / sqrt(tot);
+    if (AT(y, jm) < 0) sc = -sc;
+    a.scale[q] = sc;
+  }
+#undef AT
+}
+
 // Q[:, qcol0 + q] = scale[q] * y[:, q] placed at the vector's block rows, zero elsewhere;
 // 32 x 32 tiles transposed through shared memory (coalesced on both sides).
 __global__ void td_place_vectors(const double* y, const double* scale, int64_t nvec, int64_t col0,
                                  const int64_t* vs0, const int64_t* vm, int64_t n, double* Q, int64_t ldq,
-                                 int64_t qcol0) {
+                                 int64_t qcol0, const unsigned char* single, int mode) {
   __shared__ double tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32, v0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
@@ -336,7 +491,7 @@ __global__ void td_place_vectors(const double* y, const double* scale, int64_t n
   __syncthreads();
   for (int vv = ty; vv < 32; vv += 8) {
     const int64_t v = v0 + vv, row = r0 + tx;
-    if (v < nvec && row < n) Q[SK_IDX(row, qcol0 + v, ldq)] = tile[tx][vv];
+    if (v < nvec && row < n && single[col0 + v] == mode) Q[SK_IDX(row, qcol0 + v, ldq)] = tile[tx][vv];
   }
 }
 
@@ -717,6 +872,7 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
   w.lamv = ar.take<double>(ne);
   w.gblk = ar.take<double>(ne);
   w.vblk = ar.take<int64_t>(2 * ne);
+  w.single = ar.take<unsigned char>(ne);
   // bound the interleaved LU workspace: 16 GiB up to n = 40000, 4 GiB beyond (n = 65536 with
   // vectors on 4 GPUs must fit next to A, the reflector stores and X in 178 GiB)
   const int64_t lu_cap = (nn > 40000) ? (4ll << 30) : (16ll << 30);
@@ -865,6 +1021,12 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
   double gmax = 0.0;
   for (double g : gb) gmax = std::max(gmax, g);
   for (int64_t i = 1; i < nev; i++) clus_start[i] = (lam[i - 1] - lam[i] < 1e-6 * gmax) ? clus_start[i - 1] : i;
+  // isolated eigenvalues (a cluster of one, no dstein perturbation) take the twisted
+  // factorization; cluster members keep dstein's iterated solves with random start vectors
+  std::vector<unsigned char> single(nev);
+  for (int64_t i = 0; i < nev; i++)
+    single[i] = (clus_start[i] == i && (i + 1 == nev || clus_start[i + 1] == i + 1) && lv[i] == lam[i]) ? 1 : 0;
+  cudaMemcpyAsync(w.single, single.data(), (size_t)nev, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(w.lamv, lv.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(w.gblk, gv.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(w.vblk, vb.data(), sizeof(int64_t) * 2 * nev, cudaMemcpyHostToDevice, st);
@@ -875,21 +1037,39 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
   const int64_t vhi = k1v;
   int64_t vlo = std::min<int64_t>(std::max<int64_t>(0, k0v - W), clus_start[k0v]);
   if (vlo_out) *vlo_out = vlo;
-  for (int64_t c0 = vlo; c0 < vhi; c0 += w.batch) {
-    int64_t nb = std::min(w.batch, vhi - c0);
-    InvArgs a;
-    a.alpha = alpha_d; a.vs0 = w.vblk; a.vm = w.vblk + nev; a.lam = w.lamv; a.gblk = w.gblk;
-    a.nvec = nb; a.col0 = c0;
-    size_t stride = (size_t)n * nb;
-    a.wa = w.inv; a.wb = w.inv + stride; a.wc = w.inv + 2 * stride; a.wd = w.inv + 3 * stride; a.y = w.inv + 4 * stride;
-    a.scale = w.inv + 5 * stride;
-    a.win = w.inv_in; a.seed = prm.seed; a.nfail = w.nfail;
-    KScope ks(KC_TRID_INV, st, 2);
-    // one warp per CTA: the latency-bound per-vector chains spread over every SM (per-SM
-    // outstanding-load capacity, not the thread count, limits this kernel)
-    td_inverse_kernel<8><<<(unsigned)((nb + 31) / 32), 32, 0, st>>>(a);
-    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((nb + 31) / 32));
-    td_place_vectors<<<grid, dim3(32, 8), 0, st>>>(a.y, a.scale, nb, c0, w.vblk, w.vblk + nev, n, Q, ldq, c0 - vlo);
+  // pass 0: cluster members by dstein (batches sized for its five LU arrays); pass 1: isolated
+  // eigenvalues by the twisted factorization (three arrays: 5/3 larger batches in the same
+  // workspace, one batch at n = 32768)
+  const int64_t batch_t = std::max<int64_t>(1, std::min<int64_t>(nev, (5 * w.batch) / 3 - 1));   // 3 n bt + bt <= 5 n batch
+  for (int pass = 0; pass < 2; pass++) {
+    const int64_t bsz = pass ? batch_t : w.batch;
+    for (int64_t c0 = vlo; c0 < vhi; c0 += bsz) {
+      int64_t nb = std::min(bsz, vhi - c0);
+      bool any = false;
+      for (int64_t v = c0; v < c0 + nb && !any; v++) any = (single[v] == pass);
+      if (!any) continue;
+      InvArgs a;
+      a.alpha = alpha_d; a.vs0 = w.vblk; a.vm = w.vblk + nev; a.lam = w.lamv; a.gblk = w.gblk;
+      a.nvec = nb; a.col0 = c0;
+      size_t stride = (size_t)n * nb;
+      if (pass == 0) {
+        a.wa = w.inv; a.wb = w.inv + stride; a.wc = w.inv + 2 * stride; a.wd = w.inv + 3 * stride;
+        a.y = w.inv + 4 * stride; a.scale = w.inv + 5 * stride;
+      } else {
+        a.wa = w.inv; a.wb = w.inv + stride; a.wc = nullptr; a.wd = nullptr;
+        a.y = w.inv + 2 * stride; a.scale = w.inv + 3 * stride;
+      }
+      a.win = w.inv_in; a.seed = prm.seed; a.nfail = w.nfail;
+      a.single = w.single; a.pivmin = pivmin;
+      KScope ks(KC_TRID_INV, st, 2);
+      // one warp per CTA: the latency-bound per-vector chains spread over every SM (per-SM
+      // outstanding-load capacity, not the thread count, limits these kernels)
+      if (pass == 0) td_inverse_kernel<8><<<(unsigned)((nb + 31) / 32), 32, 0, st>>>(a);
+      else td_twisted_kernel<<<(unsigned)((nb + 15) / 16), 32, 0, st>>>(a);
+      dim3 grid((unsigned)((n + 31) / 32), (unsigned)((nb + 31) / 32));
+      td_place_vectors<<<grid, dim3(32, 8), 0, st>>>(a.y, a.scale, nb, c0, w.vblk, w.vblk + nev, n, Q, ldq, c0 - vlo,
+                                                     w.single, pass);
+    }
   }
   e = cudaGetLastError();
   if (e) return e;
