@@ -419,12 +419,17 @@ __global__ void __launch_bounds__(128) td_twisted_kernel(InvArgs a) {
       AT(y, r) = 1.0;
       ssq = 1.0; zmax = 1.0;
       for (int64_t kb = r - 1; kb >= 0; kb -= 16) {
-        double mu[16];
+        // all 16 loads first (a division's slow-path branch would otherwise keep the next
+        // load behind it), then the 16 independent divisions
+        double mu[16], dv[16], nv[16];
 #pragma unroll
         for (int u = 0; u < 16; u++) {
           const int64_t k = kb - u;
-          mu[u] = (k >= 0) ? -(al[k] / AT(D, k)) : 0.0;
+          dv[u] = (k >= 0) ? AT(D, k) : 1.0;
+          nv[u] = (k >= 0) ? al[k] : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 16; u++) mu[u] = -(nv[u] / dv[u]);
 #pragma unroll
         for (int u = 0; u < 16; u++) {
           const int64_t k = kb - u;
@@ -438,12 +443,15 @@ __global__ void __launch_bounds__(128) td_twisted_kernel(InvArgs a) {
     } else {
       double z = 1.0;
       for (int64_t kb = r + 1; kb < m; kb += 16) {
-        double mu[16];
+        double mu[16], dv[16], nv[16];
 #pragma unroll
         for (int u = 0; u < 16; u++) {
           const int64_t k = kb + u;
-          mu[u] = (k < m) ? -(al[k - 1] / AT(E, k)) : 0.0;
+          dv[u] = (k < m) ? AT(E, k) : 1.0;
+          nv[u] = (k < m) ? al[k - 1] : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 16; u++) mu[u] = -(nv[u] / dv[u]);
 #pragma unroll
         for (int u = 0; u < 16; u++) {
           const int64_t k = kb + u;
