@@ -165,11 +165,14 @@ struct B2TWork {
   unsigned long long* prog = nullptr;   // BT2 wavefront: per CTA x producer warp progress
 };
 
+constexpr int kCountGrid = 131072;   // max points of the bisection start grid
+
 struct TridWork {
   double* a2 = nullptr;        // alpha^2 (n)
   double* lamc = nullptr;      // candidates (n + padding)
   double* gtask = nullptr;     // Gershgorin bound per bisection task (n)
   int64_t* tsk = nullptr;      // 3 * n task arrays
+  int* cgrid = nullptr;        // Sturm counts on the bisection start grid (kCountGrid + 1)
   double* lamv = nullptr;      // per-vector perturbed lambda (nev)
   double* gblk = nullptr;      // per-vector block bound
   int64_t* vblk = nullptr;     // 2 * nev (s0, m)

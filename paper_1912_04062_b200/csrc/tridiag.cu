@@ -92,10 +92,25 @@ __device__ __forceinline__ int td_sturm32(const double* __restrict__ a2, int64_t
   return cnt;
 }
 
+// Count grid (one unreduced block): c[j] = Sturm count at x_j = -bnd + 2 bnd j / M, j = 1..M-1
+// (c[0] = 0 and c[M] = m are implicit: the Gershgorin bound).  One pass of M counts, the
+// cost of one multisection round, replaces the first ~log_{K+1}(M) rounds of every eigenvalue:
+// each starts from the grid cell [x_{j-1}, x_j) where the count crosses its index.
+__device__ __forceinline__ double td_grid_x(double bnd, int j, int M) { return -bnd + (2.0 * bnd) * ((double)j / (double)M); }
+__device__ __forceinline__ double td_bnd(double g, double pivmin) { return g * (1.0 + 4.0 * DBL_EPSILON) + 4.0 * pivmin; }
+
+__global__ void __launch_bounds__(128) td_count_grid_kernel(const double* a2, int64_t s0, int m, double g, int M,
+                                                            double pivmin, int* cgrid) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < 1 || j >= M) return;
+  cgrid[j] = td_sturm32(a2, s0, m, td_grid_x(td_bnd(g, pivmin), j, M), pivmin);
+}
+
 template <int K>
-__global__ void __launch_bounds__(128) td_msect_kernel(const double* a2, const int64_t* task_s0, const int64_t* task_m,
+__global__ void __launch_bounds__(128, 7) td_msect_kernel(const double* a2, const int64_t* task_s0, const int64_t* task_m,
                                                        const int64_t* task_i, const double* task_g, int64_t q0,
-                                                       int64_t q1, double pivmin, double* out) {
+                                                       int64_t q1, double pivmin, double* out, const int* cgrid,
+                                                       int M) {
   static_assert(32 % K == 0, "K divides the warp");
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, k = lane % K, gbase = lane - k;
@@ -105,8 +120,18 @@ __global__ void __launch_bounds__(128) td_msect_kernel(const double* a2, const i
   const int64_t s0 = task_s0[qq];
   const int m = (int)task_m[qq], i = (int)task_i[qq];
   const double g = task_g[qq];
-  const double bnd = g * (1.0 + 4.0 * DBL_EPSILON) + 4.0 * pivmin;
+  const double bnd = td_bnd(g, pivmin);
   double lo = -bnd, hi = bnd;
+  if (M > 1 && valid) {
+    // grid cell of index i: jl < jh with count(x_jl) <= i < count(x_jh), c[0] = 0, c[M] = m
+    int jl = 0, jh = M;
+    while (jh - jl > 1) {
+      const int jm = (jl + jh) >> 1;
+      if (__ldg(cgrid + jm) > i) jh = jm; else jl = jm;
+    }
+    if (jl > 0) lo = td_grid_x(bnd, jl, M);
+    if (jh < M) hi = td_grid_x(bnd, jh, M);
+  }
   const double atol = DBL_EPSILON * g;
   bool done = !valid || m == 1;
   for (int it = 0; it < 400; it++) {
@@ -875,6 +900,7 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
   w.lamc = ar.take<double>(nn + 1024);   // + all-gather padding (<= one slice per rank)
   w.gtask = ar.take<double>(nn);
   w.tsk = ar.take<int64_t>(3 * nn);
+  w.cgrid = ar.take<int>(kCountGrid + 1);
   if (!vectors) return;
   int64_t ne = std::max<int64_t>(nev, 1);
   w.lamv = ar.take<double>(ne);
@@ -983,11 +1009,21 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
       const int64_t slots = (int64_t)nsm * 1024, nt = qb - qa;
       int K = (nt * 32 <= slots) ? 32 : (nt * 16 <= slots) ? 16 : 8;
       if (const char* v = getenv("SKEWEIG_MSECT_K")) K = atoi(v) == 32 ? 32 : atoi(v) == 16 ? 16 : 8;   // experiments
+      // count grid for a single unreduced block (the generic case): ~one round's worth of counts
+      int M = 0;
+      if (nblk == 1 && n >= 4 && nt > 0) {
+        M = (int)std::min<int64_t>(kCountGrid, std::max<int64_t>(256, 8 * n));
+        if (const char* v = getenv("SKEWEIG_COUNT_GRID")) M = std::min(kCountGrid, std::max(0, atoi(v)));   // experiments
+        if (M > 1)
+          td_count_grid_kernel<<<(unsigned)((M + 127) / 128), 128, 0, st>>>(w.a2, 0, (int)n, gb[0], M, pivmin, w.cgrid);
+      }
       if (nt > 0) {
         const unsigned grid = (unsigned)((nt * K + 127) / 128);
-        if (K == 32) td_msect_kernel<32><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc);
-        else if (K == 16) td_msect_kernel<16><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc);
-        else td_msect_kernel<8><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc);
+        if (K == 32)
+          td_msect_kernel<32><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M);
+        else if (K == 16)
+          td_msect_kernel<16><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M);
+        else td_msect_kernel<8><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M);
       }
     }
     if (P > 1) {
