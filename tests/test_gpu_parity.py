@@ -232,6 +232,38 @@ def test_tridiag_stage_vs_oracle(sk, n):
     assert np.max(np.abs(Q.T @ Q - np.eye(nev))) <= 1e-11
 
 
+@pytest.mark.parametrize("case", ["random", "split", "graded", "glued"])
+@pytest.mark.parametrize("grid", ["0", "default"])
+def test_tridiag_start_grid_vs_oracle(sk, case, grid, monkeypatch):
+    """Bisection from the Sturm-count start grid (one unreduced block) and from the Gershgorin
+    interval (SKEWEIG_COUNT_GRID=0; also the path of a split matrix): eigenvalues against the
+    oracle's plain bisection, vectors by residual and orthogonality (R9)."""
+    n = 1531
+    a = skewgen.uniform_pm1(np.arange(n - 1, dtype=np.uint64) + np.uint64(7 * n))
+    if case == "split":
+        a[[100, 101, 700]] = 0.0                       # three unreduced blocks, one of size 1
+    elif case == "graded":
+        a = a * np.logspace(0, -12, n - 1)             # eigenvalues over 12 decades
+    elif case == "glued":
+        a = np.abs(a) + 1.0
+        a[n // 2] = 1e-9                               # two nearly decoupled halves: close pairs
+    if grid == "0":
+        monkeypatch.setenv("SKEWEIG_COUNT_GRID", "0")
+    else:
+        monkeypatch.delenv("SKEWEIG_COUNT_GRID", raising=False)
+    nev = n // 2
+    lam_o, _, _ = oracle.tridiag_eig(a, nev, want_vectors=False)
+    ctx = sk.Context()
+    lam, Q = sk.tridiag_eig(torch.from_numpy(a).cuda(), nev, ctx=ctx)
+    lam, Q = lam.cpu().numpy(), Q.cpu().numpy()
+    g = 2 * np.max(np.abs(a))
+    assert np.all(np.diff(lam) <= 0)
+    assert np.max(np.abs(lam - lam_o)) <= 100 * n * EPS * g
+    Tm = np.diag(a, 1) + np.diag(a, -1)
+    assert np.max(np.linalg.norm(Tm @ Q - Q * lam, axis=0)) <= 50 * n * EPS * g
+    assert np.max(np.abs(Q.T @ Q - np.eye(nev))) <= 1e-11
+
+
 # ------------------------------------------------------------------ BSE entry point
 @pytest.mark.parametrize("n", [2, 64, 256])
 def test_bse_vs_oracle(sk, n):
