@@ -123,6 +123,14 @@ static bool is_device_ptr(const void* p) {
   if (e != cudaSuccess) { cudaGetLastError(); return false; }
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory: asynchronous copies overlap kernels
+static bool is_pinned_host(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeHost;
+}
 
 
 }  // namespace sk
@@ -390,6 +398,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   cudaStream_t st = c.stream;
   const int64_t n = p.n;
   const bool vec = (Zre != nullptr);
+  bool re_early = false;   // real parts downloaded during BT1 of the imaginary parts
   if (vec && p.f2b.npanel > 0) CK(bt1_upload_meta(p.f2b, p.b1, st), "bt1 meta");
   if ((vec || c.nranks > 1) && !c.aux) {
     int lo = 0, hi = 0;
@@ -450,7 +459,20 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
     CK(bt2_apply(p.b2t, p.bw, p.X, p.ldn, 2 * nloc, st), "bt2");
     tstop(ctx, ST_BT2);
     tstart(ctx, ST_BT1);
-    if (p.f2b.npanel > 0) CK(bt1_apply(p.f2b, p.vstore, p.fw.tau, p.fw.T, p.X, p.ldn, 2 * nloc, p.b1, st), "bt1");
+    // pinned host Z: BT1 on the real parts, whose download (on the auxiliary stream) then
+    // overlaps BT1 on the imaginary parts (the column halves are independent: X <- Q1 X)
+    re_early = z_host && write_z && p.f2b.npanel > 0 && is_pinned_host(Zre) && !getenv("SKEWEIG_NO_OUT_OVERLAP");
+    if (re_early) {
+      CK(bt1_apply(p.f2b, p.vstore, p.fw.tau, p.fw.T, p.X, p.ldn, nloc, p.b1, st), "bt1 (real parts)");
+      CK(cudaEventRecord(c.ev_fork, st), "fork");
+      CK(cudaStreamWaitEvent(c.aux, c.ev_fork, 0), "fork wait");
+      CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost, c.aux), "Zre out");
+      CK(cudaEventRecord(c.ev_join, c.aux), "join");
+      CK(bt1_apply(p.f2b, p.vstore, p.fw.tau, p.fw.T, p.X + (size_t)p.ldn * nloc, p.ldn, nloc, p.b1, st),
+         "bt1 (imaginary parts)");
+    } else if (p.f2b.npanel > 0) {
+      CK(bt1_apply(p.f2b, p.vstore, p.fw.tau, p.fw.T, p.X, p.ldn, 2 * nloc, p.b1, st), "bt1");
+    }
     tstop(ctx, ST_BT1);
   }
   // ---- output
@@ -459,9 +481,11 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
                      st), "lambda out");
   if (vec && write_z) {
     if (z_host) {
-      CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost, st), "Zre out");
+      if (!re_early)
+        CK(cudaMemcpy2DAsync(Zre, ldz * 8, p.X, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost, st), "Zre out");
       CK(cudaMemcpy2DAsync(Zim, ldz * 8, p.X + (size_t)p.ldn * nloc, p.ldn * 8, n * 8, nloc, cudaMemcpyDeviceToHost,
                            st), "Zim out");
+      if (re_early) CK(cudaStreamWaitEvent(st, c.ev_join, 0), "join wait");
     } else {
       CK(split_output(p.X, p.ldn, n, nloc, Zre, Zim, ldz, st), "split output");
     }

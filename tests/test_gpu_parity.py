@@ -147,6 +147,28 @@ def test_host_pointer_entry_matches_device(sk):
     assert np.array_equal(A, skewgen.random_skew_lower_colmajor(n, 21))
 
 
+def test_pinned_host_output_overlap_matches_device(sk):
+    """Pinned host Z: BT1 runs on the real parts first and their download overlaps BT1 on the
+    imaginary parts (api.cu solve_core); the result equals the device-resident solve."""
+    n, nev = 700, 350
+    A = torch.from_numpy(skewgen.random_skew_lower_colmajor(n, 33))
+    Ah = torch.empty((n, n), dtype=torch.float64, pin_memory=True).t()
+    Ah.copy_(A)
+    lam_h = torch.empty(nev, dtype=torch.float64, pin_memory=True)
+    Zre_h = torch.empty((nev, n), dtype=torch.float64, pin_memory=True).t()
+    Zim_h = torch.empty((nev, n), dtype=torch.float64, pin_memory=True).t()
+    ctx = sk.Context()
+    sk.skew_eig_host_range(Ah, nev, 0, nev, lam_h, Zre_h, Zim_h, ctx=ctx)
+    lam, Zre, Zim = sk.skew_eig(A.cuda(), nev, ctx=ctx)
+    assert torch.equal(lam_h, lam.cpu())
+    scale = Zre_h.abs().max().item()
+    assert (Zre_h - Zre.cpu()).abs().max().item() <= 1e-13 * scale
+    assert (Zim_h - Zim.cpu()).abs().max().item() <= 1e-13 * scale
+    Afull = skewgen.random_skew(n, 33)
+    lam_o, Zre_o, Zim_o, _ = oracle.skew_eig(Afull)
+    _check_pairs(Afull, lam_h.numpy(), Zre_h.numpy(), Zim_h.numpy(), lam_o, Zre_o, Zim_o)
+
+
 def test_bad_arguments(sk):
     import ctypes
     L = sk.lib()
