@@ -41,8 +41,10 @@ int skew_stage_tridiag_eig(skew_ctx ctx, int64_t n, const double* alpha, int64_t
  * one of SKEW_KERNEL_CLASSES classes (skew_kernel_class_name); skew_kernel_stats
  * returns, for the last call, the number of launches per class and -- when
  * profiling is on -- the summed device time (ms) of each class measured with CUDA
- * events recorded on the context stream around the launches. */
-#define SKEW_KERNEL_CLASSES 20
+ * events recorded on the context stream around the launches.  The last class,
+ * "collectives", times the NCCL / virtual-group collectives of a distributed solve
+ * (panel broadcast, skew-SYMM allreduce, band allreduce, eigenvalue allgather). */
+#define SKEW_KERNEL_CLASSES 21
 int skew_set_profiling(skew_ctx ctx, int on);
 int skew_kernel_stats(skew_ctx ctx, double* ms_out, int64_t* launches_out, int count);
 const char* skew_kernel_class_name(int cls);

@@ -68,7 +68,7 @@ EXPORTS = {
     "skew_kernel_stats": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), ctypes.c_int], ctypes.c_int),
     "skew_kernel_class_name": ([ctypes.c_int], ctypes.c_char_p),
 }
-KERNEL_CLASSES = 20
+KERNEL_CLASSES = 21
 
 STAGES = ["f2b", "b2t", "tridiag", "bt2", "bt1", "output", "bse"]
 

@@ -178,7 +178,7 @@ static void kcollect(skew_ctx ctx) {
 static const char* kNames[KC_COUNT] = {"panel_qr", "vt", "skew_symm", "w_correction", "skew_r2k", "band_extract",
                                        "bulge_chase", "bisection", "inverse_iteration", "reorth", "assemble_D",
                                        "bt2_tbuild", "bt2_apply", "bt1_prep", "bt1_z", "bt1_update", "output", "bse",
-                                       "onestep_skew_mv", "onestep_column"};
+                                       "onestep_skew_mv", "onestep_column", "collectives"};
 
 extern "C" {
 
@@ -428,6 +428,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
   tstart(ctx, ST_B2T);
   CK(band_extract(A_d, lda, n, c.prm.b, p.bw.AB, p.b2t.ldab, st, d.P, d.rank), "band extract");
   if (d.P > 1) {   // every rank contributed the band columns it owns
+    KScope ks(KC_COLL, st);
     const int r = coll_allreduce_sum(d, p.bw.AB, (size_t)p.b2t.ldab * n, st);
     if (r) { c.last_error = std::string("band allreduce: ") + coll_error_string(d, r); return SKEW_ERR_NCCL; }
   }

@@ -1286,6 +1286,7 @@ cudaError_t f2b_update(const F2BLayout& L, int64_t j, double* A, int64_t lda, do
     }
   }
   if (d.P > 1) {   // Y = sum over ranks of the partial skew-SYMM products (NVLink allreduce)
+    KScope ks(KC_COLL, st);
     const int r = coll_allreduce_sum(d, Wp, (size_t)ldn * b, st);
     if (r) { *nccl_err = r; return cudaErrorUnknown; }
   }
@@ -1368,6 +1369,7 @@ cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, 
     if (d.P > 1) {
       const int64_t g = j / L.merge, pl = j % L.merge;
       double* Vcols = vstore + L.goff[g] + pl * (int64_t)L.b * L.gld[g];   // the panel's columns of the group block
+      KScope ks(KC_COLL, st);
       int r = coll_group_start(d);
       if (!r) r = coll_bcast(d, Vcols, sizeof(double) * (size_t)L.gld[g] * L.b, owner, st);
       if (!r) r = coll_bcast(d, w.T + j * (int64_t)L.b * L.b, sizeof(double) * (size_t)L.b * L.b, owner, st);

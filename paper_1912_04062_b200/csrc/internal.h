@@ -85,7 +85,7 @@ struct F2BLayout {
 // launching stream (skew_kernel_stats).
 enum KClass {
   KC_PANEL = 0, KC_VT, KC_SYMM, KC_WCORR, KC_R2K, KC_BAND, KC_CHASE, KC_TRID_BISECT, KC_TRID_INV, KC_TRID_REORTH,
-  KC_ASSEMBLE, KC_BT2_T, KC_BT2, KC_BT1_PREP, KC_BT1_Z, KC_BT1_UPD, KC_OUT, KC_BSE, KC_OS_MV, KC_OS_COL, KC_COUNT
+  KC_ASSEMBLE, KC_BT2_T, KC_BT2, KC_BT1_PREP, KC_BT1_Z, KC_BT1_UPD, KC_OUT, KC_BSE, KC_OS_MV, KC_OS_COL, KC_COLL, KC_COUNT
 };
 struct Prof {
   bool on = false;

@@ -1027,6 +1027,7 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
       }
     }
     if (P > 1) {
+      KScope ks(KC_COLL, st);
       if (coll_allgather(*d, w.lamc, (size_t)cnt, st)) return cudaErrorUnknown;
     }
     e = cudaMemcpyAsync(lamc.data(), w.lamc, sizeof(double) * ntask, cudaMemcpyDeviceToHost, st);
