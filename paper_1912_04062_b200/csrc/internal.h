@@ -173,6 +173,7 @@ struct TridWork {
   double* gtask = nullptr;     // Gershgorin bound per bisection task (n)
   int64_t* tsk = nullptr;      // 3 * n task arrays
   int* cgrid = nullptr;        // Sturm counts on the bisection start grid (kCountGrid + 1)
+  double* scal = nullptr;      // device scalars: g, pivmin, #zeros in alpha, first ghost vector
   double* lamv = nullptr;      // per-vector perturbed lambda (nev)
   double* gblk = nullptr;      // per-vector block bound
   int64_t* vblk = nullptr;     // 2 * nev (s0, m)

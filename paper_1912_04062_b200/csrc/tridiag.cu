@@ -110,16 +110,18 @@ template <int K>
 __global__ void __launch_bounds__(128, 7) td_msect_kernel(const double* a2, const int64_t* task_s0, const int64_t* task_m,
                                                        const int64_t* task_i, const double* task_g, int64_t q0,
                                                        int64_t q1, double pivmin, double* out, const int* cgrid,
-                                                       int M) {
+                                                       int M, int64_t n1, double g1) {
   static_assert(32 % K == 0, "K divides the warp");
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, k = lane % K, gbase = lane - k;
   const int64_t q = q0 + gt / K;
   const bool valid = q < q1;
   const int64_t qq = valid ? q : q1 - 1;
-  const int64_t s0 = task_s0[qq];
-  const int m = (int)task_m[qq], i = (int)task_i[qq];
-  const double g = task_g[qq];
+  // task list, or (task_s0 == null) one unreduced block of order n1: task q = index n1-1-q
+  const int64_t s0 = task_s0 ? task_s0[qq] : 0;
+  const int m = task_s0 ? (int)task_m[qq] : (int)n1;
+  const int i = task_s0 ? (int)task_i[qq] : (int)(n1 - 1 - qq);
+  const double g = task_s0 ? task_g[qq] : g1;
   const double bnd = td_bnd(g, pivmin);
   double lo = -bnd, hi = bnd;
   if (M > 1 && valid) {
@@ -512,10 +514,12 @@ __global__ void td_place_vectors(const double* y, const double* scale, int64_t n
   __shared__ double tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32, v0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  const bool mine = v0 + tx < nvec && single[col0 + v0 + tx] == mode;   // this pass computed vector v0+tx
+  if (!__syncthreads_or(mine)) return;
   for (int rr = ty; rr < 32; rr += 8) {
     const int64_t row = r0 + rr, v = v0 + tx;
     double val = 0.0;
-    if (v < nvec && row < n) {
+    if (mine && row < n) {
       const int64_t s0 = vs0[col0 + v], m = vm[col0 + v];
       if (row >= s0 && row < s0 + m) val = y[(size_t)(row - s0) * nvec + v] * scale[v];
     }
@@ -901,6 +905,7 @@ void trid_reserve(Arena& ar, int64_t n, int64_t nev, bool vectors, TridWork& w, 
   w.gtask = ar.take<double>(nn);
   w.tsk = ar.take<int64_t>(3 * nn);
   w.cgrid = ar.take<int>(kCountGrid + 1);
+  w.scal = ar.take<double>(8);
   if (!vectors) return;
   int64_t ne = std::max<int64_t>(nev, 1);
   w.lamv = ar.take<double>(ne);
@@ -940,13 +945,122 @@ static cudaError_t reorth_project(const double* Qp, int64_t ldq, int p, double* 
   return cudaGetLastError();
 }
 
-// lam (nev, descending, device out); Q (n x nev, ldq) or null.
-cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q, int64_t ldq,
-                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st, int64_t k0v, int64_t k1v,
-                     int64_t* vlo_out, const Dist* d) {
+// ---- device-side bookkeeping (one unreduced block, i.e. no exact zero in alpha)
+// scal[0] = Gershgorin bound g, scal[1] = pivmin = DBL_MIN max(1, max alpha^2), scal[2] =
+// number of exact zeros in alpha; a2 = alpha^2 (a2[n-1] = 0).  The same arithmetic as the
+// host path (same max / sum order is irrelevant: maxima are exact).
+__global__ void __launch_bounds__(1024) td_prep_kernel(const double* alpha, int64_t n, double* a2, double* scal) {
+  __shared__ double sg[32], sa[32];
+  __shared__ int sz[32];
+  double gm = 0.0, am = 0.0;
+  int nz = 0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const double ak = (k + 1 < n) ? alpha[k] : 0.0;
+    a2[k] = ak * ak;
+    am = fmax(am, ak * ak);
+    nz += (k + 1 < n && ak == 0.0) ? 1 : 0;
+    gm = fmax(gm, (k > 0 ? fabs(alpha[k - 1]) : 0.0) + fabs(ak));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
+    nz += __shfl_xor_sync(0xffffffffu, nz, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { sg[warp] = gm; sa[warp] = am; sz[warp] = nz; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    gm = lane < nw ? sg[lane] : 0.0;
+    am = lane < nw ? sa[lane] : 0.0;
+    nz = lane < nw ? sz[lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+      am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
+      nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    }
+    if (lane == 0) { scal[0] = gm; scal[1] = DBL_MIN * fmax(1.0, am); scal[2] = (double)nz; }
+  }
+}
+
+// Per-vector data of the inverse-iteration / twisted stage from the descending eigenvalues of
+// one block, the device version of the host loops (R9): dstein's perturbation
+// lambda_k <- lambda_{k-1} - 10 eps g (sequential inside a run of close values; a run can only
+// continue across a gap < nev * 10 eps g, so threads start at the gaps above that and walk),
+// clusters (gap < 1e-6 g: a max-scan of the cluster starts), isolated flags, the first ghost
+// vector vlo = min(k0 - W, cluster start of k0) and the re-orthogonalisation block list.
+struct VecPrepArgs {
+  const double* lam; int64_t nev; int64_t n; double g;
+  double* lv; double* gv; int64_t* vb; unsigned char* single; int64_t* cs;
+  int64_t k0v, k1v; int W; int64_t* rblk; int64_t* vlo;
+};
+__global__ void __launch_bounds__(1024) td_vecprep_kernel(VecPrepArgs a) {
+  __shared__ int64_t part[1024];
+  const int T = blockDim.x, t = threadIdx.x;
+  const int64_t nev = a.nev, C = (nev + T - 1) / T;
+  const int64_t i0 = smin<int64_t>(nev, (int64_t)t * C), i1 = smin<int64_t>(nev, i0 + C);
+  const double del = 10.0 * DBL_EPSILON * a.g, thr = 1e-6 * a.g, brk = (double)nev * del;
+  // cluster starts: cs[i] = the last i' <= i with i' == 0 or lam[i'-1] - lam[i'] >= thr
+  int64_t last = -1;
+  for (int64_t i = i0; i < i1; i++)
+    if (i == 0 || !(a.lam[i - 1] - a.lam[i] < thr)) last = i;
+  part[t] = last;
+  __syncthreads();
+  for (int o = 1; o < T; o <<= 1) {   // inclusive max-scan of the chunk summaries
+    const int64_t v = (t >= o) ? part[t - o] : -1;
+    __syncthreads();
+    part[t] = smax<int64_t>(part[t], v);
+    __syncthreads();
+  }
+  int64_t run = (t > 0) ? part[t - 1] : -1;
+  for (int64_t i = i0; i < i1; i++) {
+    if (i == 0 || !(a.lam[i - 1] - a.lam[i] < thr)) run = i;
+    a.cs[i] = run;
+    a.gv[i] = a.g;
+    a.vb[i] = 0;
+    a.vb[nev + i] = a.n;
+  }
+  // perturbation, sequential within runs (bit-identical to the host loop)
+  for (int64_t i = i0; i < i1; i++) {
+    if (!(i == 0 || !(a.lam[i - 1] - a.lam[i] < brk))) continue;
+    double lastv = a.lam[i];
+    a.lv[i] = lastv;
+    for (int64_t j = i + 1; j < nev && a.lam[j - 1] - a.lam[j] < brk; j++) {
+      double x = a.lam[j];
+      if (lastv - x < del) x = lastv - del;
+      a.lv[j] = x;
+      lastv = x;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = t; i < nev; i += T)
+    a.single[i] = (a.cs[i] == i && (i + 1 == nev || a.cs[i + 1] == i + 1) && a.lv[i] == a.lam[i]) ? 1 : 0;
+  const int64_t vlo = smin<int64_t>(smax<int64_t>(0, a.k0v - a.W), a.cs[a.k0v]);
+  if (t == 0) *a.vlo = vlo;
+  for (int64_t q = t; vlo + q * kReorthNB < a.k1v; q += T) {
+    const int64_t k0 = vlo + q * kReorthNB;
+    int64_t p0 = smax<int64_t>(vlo, k0 - a.W);
+    const int64_t c = smax<int64_t>(vlo, a.cs[k0]);
+    if (c < p0) p0 = c;
+    a.rblk[3 * q] = k0 - vlo;
+    a.rblk[3 * q + 1] = p0 - vlo;
+    a.rblk[3 * q + 2] = smin<int64_t>(kReorthNB, a.k1v - k0);
+  }
+}
+
+static cudaError_t trid_vectors(int64_t n, const double* alpha_d, int64_t nev, double* Q, int64_t ldq, TridWork& w,
+                                const Params& prm, cudaStream_t st, int64_t vlo, int64_t vhi, double pivmin,
+                                const std::vector<int64_t>* clus_host, bool blk_on_device, int64_t* nfail_out);
+
+// Host path of the tridiagonal stage, for a matrix that splits into unreduced blocks (an exact
+// zero in alpha): per-block Gershgorin intervals and tasks, selection of the top nev, dstein's
+// per-block perturbation, clusters -- then the shared vector stage.
+static cudaError_t trid_run_host(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q,
+                                 int64_t ldq, TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st,
+                                 int64_t k0v, int64_t k1v, int64_t* vlo_out, const Dist* d) {
   cudaError_t e;
-  *nfail_out = 0;
-  if (nev <= 0) return cudaSuccess;
   // alpha to host (n-1 doubles): split points, Gershgorin bounds, task lists
   std::vector<double> al(std::max<int64_t>(n - 1, 1), 0.0);
   if (n > 1) {
@@ -1020,10 +1134,10 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
       if (nt > 0) {
         const unsigned grid = (unsigned)((nt * K + 127) / 128);
         if (K == 32)
-          td_msect_kernel<32><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M);
+          td_msect_kernel<32><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M, 0, 0.0);
         else if (K == 16)
-          td_msect_kernel<16><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M);
-        else td_msect_kernel<8><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M);
+          td_msect_kernel<16><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M, 0, 0.0);
+        else td_msect_kernel<8><<<grid, 128, 0, st>>>(w.a2, d_s0, d_m, d_i, w.gtask, qa, qb, pivmin, w.lamc, w.cgrid, M, 0, 0.0);
       }
     }
     if (P > 1) {
@@ -1075,13 +1189,26 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
   cudaMemcpyAsync(w.lamv, lv.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(w.gblk, gv.data(), sizeof(double) * nev, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(w.vblk, vb.data(), sizeof(int64_t) * 2 * nev, cudaMemcpyHostToDevice, st);
-  cudaMemsetAsync(w.nfail, 0, sizeof(int), st);
   // vectors [vlo, vhi): the requested range [k0v, k1v) plus the reorthogonalisation window and
   // the cluster members before it (ghost vectors, discarded by the caller)
   const int W = prm.reorth_w;
-  const int64_t vhi = k1v;
   int64_t vlo = std::min<int64_t>(std::max<int64_t>(0, k0v - W), clus_start[k0v]);
   if (vlo_out) *vlo_out = vlo;
+  // the host vectors above must outlive their asynchronous copies
+  e = trid_vectors(n, alpha_d, nev, Q, ldq, w, prm, st, vlo, k1v, pivmin, &clus_start, false, nfail_out);
+  if (e) return e;
+  return cudaStreamSynchronize(st);
+}
+
+// Vector stage (shared): dstein / twisted vectors of [vlo, vhi) into Q, the re-orthogonalisation,
+// the failure count.  Needs lamv, gblk, vblk, single on the device; the cluster starts on the
+// host (clus_host) or, with blk_on_device, the re-orthogonalisation block list in w.rblk.
+static cudaError_t trid_vectors(int64_t n, const double* alpha_d, int64_t nev, double* Q, int64_t ldq, TridWork& w,
+                                const Params& prm, cudaStream_t st, int64_t vlo, int64_t vhi, double pivmin,
+                                const std::vector<int64_t>* clus_host, bool blk_on_device, int64_t* nfail_out) {
+  cudaError_t e;
+  const int W = prm.reorth_w;
+  cudaMemsetAsync(w.nfail, 0, sizeof(int), st);
   // pass 0: cluster members by dstein (batches sized for its five LU arrays); pass 1: isolated
   // eigenvalues by the twisted factorization (three arrays: 5/3 larger batches in the same
   // workspace, one batch at n = 32768)
@@ -1090,9 +1217,6 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     const int64_t bsz = pass ? batch_t : w.batch;
     for (int64_t c0 = vlo; c0 < vhi; c0 += bsz) {
       int64_t nb = std::min(bsz, vhi - c0);
-      bool any = false;
-      for (int64_t v = c0; v < c0 + nb && !any; v++) any = (single[v] == pass);
-      if (!any) continue;
       InvArgs a;
       a.alpha = alpha_d; a.vs0 = w.vblk; a.vm = w.vblk + nev; a.lam = w.lamv; a.gblk = w.gblk;
       a.nvec = nb; a.col0 = c0;
@@ -1120,6 +1244,17 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
   if (e) return e;
   if (const char* ro = getenv("SKEWEIG_REORTH_OFF"))   // experiments: the vectors as computed
     if (atoi(ro) == 1) return cudaSuccess;
+  // the cluster starts on the host (the kernel-per-step fallback, or the host path)
+  std::vector<int64_t> cs_local;
+  auto clus = [&]() -> const std::vector<int64_t>& {
+    if (clus_host) return *clus_host;
+    if (cs_local.empty()) {
+      cs_local.resize(nev);
+      cudaMemcpyAsync(cs_local.data(), w.tsk, sizeof(int64_t) * nev, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+    }
+    return cs_local;
+  };
   // re-orthogonalisation in blocks of 32 (descending order): one fused cooperative launch
   // when the per-CTA row slices fit in shared memory, else the kernel-per-step sequence
   bool fused = false;
@@ -1142,18 +1277,23 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
     }
     if (fused) {
       std::vector<int64_t> blk;
-      for (int64_t k0 = vlo; k0 < vhi; k0 += kReorthNB) {
-        int64_t p0 = std::max<int64_t>(vlo, k0 - W);
-        const int64_t cs = std::max<int64_t>(vlo, clus_start[k0]);
-        if (cs < p0) p0 = cs;
-        blk.push_back(k0 - vlo);
-        blk.push_back(p0 - vlo);
-        blk.push_back(std::min<int64_t>(kReorthNB, vhi - k0));
+      const int nblk = (int)((vhi - vlo + kReorthNB - 1) / kReorthNB);
+      if (!blk_on_device) {
+        const std::vector<int64_t>& clus_start = clus();
+        for (int64_t k0 = vlo; k0 < vhi; k0 += kReorthNB) {
+          int64_t p0 = std::max<int64_t>(vlo, k0 - W);
+          const int64_t cs = std::max<int64_t>(vlo, clus_start[k0]);
+          if (cs < p0) p0 = cs;
+          blk.push_back(k0 - vlo);
+          blk.push_back(p0 - vlo);
+          blk.push_back(std::min<int64_t>(kReorthNB, vhi - k0));
+        }
       }
-      const int nblk = (int)(blk.size() / 3);
       if (nblk > 0) {
-        e = cudaMemcpyAsync(w.rblk, blk.data(), sizeof(int64_t) * blk.size(), cudaMemcpyHostToDevice, st);
-        if (e) return e;
+        if (!blk_on_device) {
+          e = cudaMemcpyAsync(w.rblk, blk.data(), sizeof(int64_t) * blk.size(), cudaMemcpyHostToDevice, st);
+          if (e) return e;
+        }
         ReorthArgs ra;
         ra.Q = Q; ra.ldq = ldq; ra.n = n; ra.blk = w.rblk; ra.nblk = nblk; ra.part = w.rpart; ra.R = R; ra.LDR = LDR;
         ra.gbar = w.gbar;
@@ -1164,16 +1304,17 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
         KScope ks(KC_TRID_REORTH, st);
         e = cudaLaunchCooperativeKernel((void*)td_reorth_fused_kernel, dim3(G), dim3(256), args, smem, st);
         if (e) return e;
-        // the host copy of blk must outlive the async copy
-        e = cudaStreamSynchronize(st);
-        if (e) return e;
+        if (!blk_on_device) {   // the host copy of blk must outlive the async copy
+          e = cudaStreamSynchronize(st);
+          if (e) return e;
+        }
       }
     }
   }
   if (!fused) for (int64_t k0 = vlo; k0 < vhi; k0 += kReorthNB) {
     int nb = (int)std::min<int64_t>(kReorthNB, vhi - k0);
     int64_t p0 = std::max<int64_t>(vlo, k0 - W);
-    int64_t cs = std::max<int64_t>(vlo, clus_start[k0]);
+    int64_t cs = std::max<int64_t>(vlo, clus()[k0]);
     if (cs < p0) p0 = cs;
     double* Y = Q + SK_IDX(0, k0 - vlo, ldq);
     // CGS2 against [p0, k0) in chunks of <= 64 previous vectors
@@ -1204,6 +1345,79 @@ cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_
   e = cudaStreamSynchronize(st);
   *nfail_out = nf;
   return e;
+}
+
+// lam (nev, descending, device out); Q (n x nev, ldq) or null.  One unreduced block (the
+// generic case): alpha^2, the Gershgorin bound, the bisection tasks, the per-vector data and
+// the re-orthogonalisation blocks are all formed on the device; the host reads three scalars
+// (one round trip) and, for a distributed range k0v > 0, the first ghost vector.  A matrix that
+// splits (an exact zero in alpha) takes the host path above.
+cudaError_t trid_run(int64_t n, const double* alpha_d, int64_t nev, double* lam_out, double* Q, int64_t ldq,
+                     TridWork& w, const Params& prm, int64_t* nfail_out, cudaStream_t st, int64_t k0v, int64_t k1v,
+                     int64_t* vlo_out, const Dist* d) {
+  cudaError_t e;
+  *nfail_out = 0;
+  if (nev <= 0) return cudaSuccess;
+  double sc[3] = {0.0, 0.0, 1.0};
+  if (n > 1) {
+    td_prep_kernel<<<1, 1024, 0, st>>>(alpha_d, n, w.a2, w.scal);
+    e = cudaMemcpyAsync(sc, w.scal, sizeof(sc), cudaMemcpyDeviceToHost, st);
+    if (e) return e;
+    e = cudaStreamSynchronize(st);
+    if (e) return e;
+  }
+  if (n < 4 || sc[2] != 0.0 || getenv("SKEWEIG_TRID_HOST"))   // SKEWEIG_TRID_HOST: experiments
+    return trid_run_host(n, alpha_d, nev, lam_out, Q, ldq, w, prm, nfail_out, st, k0v, k1v, vlo_out, d);
+  const double g = sc[0], pivmin = sc[1];
+  const int P = d ? d->P : 1;
+  const int64_t cnt = (nev + P - 1) / P;
+  const int64_t qa = std::min<int64_t>(nev, (int64_t)(d ? d->rank : 0) * cnt), qb = std::min<int64_t>(nev, qa + cnt);
+  {
+    KScope ks(KC_TRID_BISECT, st);
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t slots = (int64_t)nsm * 1024, nt = qb - qa;
+    int K = (nt * 32 <= slots) ? 32 : (nt * 16 <= slots) ? 16 : 8;
+    if (const char* v = getenv("SKEWEIG_MSECT_K")) K = atoi(v) == 32 ? 32 : atoi(v) == 16 ? 16 : 8;   // experiments
+    int M = (int)std::min<int64_t>(kCountGrid, std::max<int64_t>(256, 8 * n));
+    if (const char* v = getenv("SKEWEIG_COUNT_GRID")) M = std::min(kCountGrid, std::max(0, atoi(v)));   // experiments
+    if (nt > 0 && M > 1)
+      td_count_grid_kernel<<<(unsigned)((M + 127) / 128), 128, 0, st>>>(w.a2, 0, (int)n, g, M, pivmin, w.cgrid);
+    if (nt > 0) {
+      const unsigned grid = (unsigned)((nt * K + 127) / 128);
+      if (K == 32)
+        td_msect_kernel<32><<<grid, 128, 0, st>>>(w.a2, nullptr, nullptr, nullptr, nullptr, qa, qb, pivmin, w.lamc,
+                                                  w.cgrid, M, n, g);
+      else if (K == 16)
+        td_msect_kernel<16><<<grid, 128, 0, st>>>(w.a2, nullptr, nullptr, nullptr, nullptr, qa, qb, pivmin, w.lamc,
+                                                  w.cgrid, M, n, g);
+      else td_msect_kernel<8><<<grid, 128, 0, st>>>(w.a2, nullptr, nullptr, nullptr, nullptr, qa, qb, pivmin, w.lamc,
+                                                    w.cgrid, M, n, g);
+    }
+  }
+  if (P > 1) {
+    KScope ks(KC_COLL, st);
+    if (coll_allgather(*d, w.lamc, (size_t)cnt, st)) return cudaErrorUnknown;
+  }
+  // one block: task q is eigenvalue n-1-q, so the candidates are already descending
+  e = cudaMemcpyAsync(lam_out, w.lamc, sizeof(double) * nev, cudaMemcpyDeviceToDevice, st);
+  if (e) return e;
+  if (!Q) return cudaSuccess;
+  VecPrepArgs va;
+  va.lam = w.lamc; va.nev = nev; va.n = n; va.g = g;
+  va.lv = w.lamv; va.gv = w.gblk; va.vb = w.vblk; va.single = w.single; va.cs = w.tsk;
+  va.k0v = k0v; va.k1v = k1v; va.W = prm.reorth_w; va.rblk = w.rblk; va.vlo = reinterpret_cast<int64_t*>(w.scal + 3);
+  td_vecprep_kernel<<<1, 1024, 0, st>>>(va);
+  int64_t vlo = 0;
+  if (k0v > 0) {   // distributed range: the ghost window reaches back to the cluster start
+    e = cudaMemcpyAsync(&vlo, w.scal + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e) return e;
+    e = cudaStreamSynchronize(st);
+    if (e) return e;
+  }
+  if (vlo_out) *vlo_out = vlo;
+  return trid_vectors(n, alpha_d, nev, Q, ldq, w, prm, st, vlo, k1v, pivmin, nullptr, true, nfail_out);
 }
 
 cudaError_t assemble_D(const double* Q, int64_t ldq, int64_t n, int64_t nev, double* X, int64_t ldx, cudaStream_t st) {

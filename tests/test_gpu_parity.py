@@ -286,6 +286,26 @@ def test_tridiag_start_grid_vs_oracle(sk, case, grid, monkeypatch):
     assert np.max(np.abs(Q.T @ Q - np.eye(nev))) <= 1e-11
 
 
+@pytest.mark.parametrize("case", ["random", "clustered"])
+def test_tridiag_device_bookkeeping_matches_host(sk, case, monkeypatch):
+    """The device-side bookkeeping of the tridiagonal stage (Gershgorin bound, pivmin, tasks,
+    dstein perturbation, clusters, isolated flags, re-orthogonalisation blocks: tridiag.cu
+    td_prep_kernel / td_vecprep_kernel) reproduces the host loops bit for bit."""
+    n = 2049
+    a = skewgen.uniform_pm1(np.arange(n - 1, dtype=np.uint64) + np.uint64(11 * n))
+    if case == "clustered":
+        a = np.abs(a) + 0.5
+        a[::7] = 1e-7          # many weakly coupled pieces: clusters and near-equal pairs
+    at = torch.from_numpy(a).cuda()
+    ctx = sk.Context()
+    monkeypatch.delenv("SKEWEIG_TRID_HOST", raising=False)
+    lam_d, Q_d = sk.tridiag_eig(at, n // 2, ctx=ctx)
+    monkeypatch.setenv("SKEWEIG_TRID_HOST", "1")
+    lam_h, Q_h = sk.tridiag_eig(at, n // 2, ctx=ctx)
+    assert torch.equal(lam_d, lam_h)
+    assert torch.equal(Q_d, Q_h)
+
+
 # ------------------------------------------------------------------ BSE entry point
 @pytest.mark.parametrize("n", [2, 64, 256])
 def test_bse_vs_oracle(sk, n):
