@@ -424,6 +424,15 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
     CK(fe, "f2b");
   }
   tstop(ctx, ST_F2B);
+  // BT1 preparation (depends on full->band only) on the auxiliary stream: already beside the
+  // chase when the chase leaves most SMs idle (small n: one CTA per active sweep), else beside
+  // the tridiagonal solve (below)
+  const bool bt1_early = vec && p.f2b.npanel > 0 && 2 * b2t_chase_ctas(n, c.prm.b, c.num_sms) <= c.num_sms;
+  if (bt1_early) {
+    CK(cudaEventRecord(c.ev_fork, st), "fork");
+    CK(cudaStreamWaitEvent(c.aux, c.ev_fork, 0), "fork wait");
+    CK(bt1_prep(p.f2b, p.vstore, p.fw.T, p.b1, c.aux), "bt1 prep");
+  }
   // ---- band -> tridiagonal
   tstart(ctx, ST_B2T);
   CK(band_extract(A_d, lda, n, c.prm.b, p.bw.AB, p.b2t.ldab, st, d.P, d.rank), "band extract");
@@ -438,7 +447,7 @@ static int solve_core(skew_ctx ctx, Plan& p, double* A_d, int64_t lda, int64_t n
     CK(cudaEventRecord(c.ev_fork, st), "fork");
     CK(cudaStreamWaitEvent(c.aux, c.ev_fork, 0), "fork wait");
     CK(bt2_prep(p.b2t, p.bw, c.aux), "bt2 prep");
-    if (p.f2b.npanel > 0) CK(bt1_prep(p.f2b, p.vstore, p.fw.T, p.b1, c.aux), "bt1 prep");
+    if (p.f2b.npanel > 0 && !bt1_early) CK(bt1_prep(p.f2b, p.vstore, p.fw.T, p.b1, c.aux), "bt1 prep");
     CK(cudaEventRecord(c.ev_join, c.aux), "join");
   }
   // ---- tridiagonal eigenproblem

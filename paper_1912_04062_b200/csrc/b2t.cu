@@ -811,6 +811,7 @@ static int chase_grid(int64_t n, int b, int nsm, int lag) {
   int64_t act = std::max<int64_t>(1, (n / std::max(b, 1)) / lag + 1);
   return (int)std::max<int64_t>(1, std::min<int64_t>(act, nsm));
 }
+int b2t_chase_ctas(int64_t n, int b, int nsm) { return n > 2 ? chase_grid(n, b, nsm, 2) : 0; }
 
 // Run the chase on w.AB (already filled, ldab = 2b+2); writes alpha and reflectors.
 cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cudaStream_t st) {

@@ -241,6 +241,7 @@ cudaError_t f2b_run(const F2BLayout& L, double* A, int64_t lda, double* vstore, 
                     cudaStream_t st, const Dist& d, int* nccl_err);
 // b2t.cu
 void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w);
+int b2t_chase_ctas(int64_t n, int b, int nsm);   // CTAs (= SMs) the chase occupies
 cudaError_t b2t_run(const B2TLayout& L, B2TWork& w, double* alpha, int nsm, cudaStream_t st);
 cudaError_t bt2_run(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, int64_t ncols, cudaStream_t st);
 cudaError_t bt2_prep(const B2TLayout& L, B2TWork& w, cudaStream_t st);   // [U | V] of every group

@@ -1262,7 +1262,8 @@ static cudaError_t trid_vectors(int64_t n, const double* alpha_d, int64_t nev, d
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int G = (int)smin<int64_t>(smin<int64_t>(nsm, kReorthMaxG), smax<int64_t>(1, (n + 7) / 8));
+    int G = (int)smin<int64_t>(smin<int64_t>(nsm, kReorthMaxG), smax<int64_t>(1, (n + 7) / 8));
+    if (const char* v = getenv("SKEWEIG_REORTH_G")) G = std::max(1, std::min(G, atoi(v)));   // experiments
     const int R = (int)((((n + G - 1) / G) + 7) & ~int64_t(7));
     const int LDR = R + (((4 - R) % 16) + 16) % 16;
     const size_t smem = ((size_t)96 * LDR + 64 * kRfHLD + 32 * 33) * sizeof(double);
