@@ -99,7 +99,7 @@ def _check(A, lams, Zre, Zim, lam_o, Zre_o, Zim_o):
         assert sin <= max(1e-9, 1e3 * EPS * n2 / gap), f"vector {k}: sin {sin:.3e} gap {gap:.3e}"
 
 
-@pytest.mark.parametrize("n,P", [(300, 2), (517, 3), (700, 4), (1090, 4)])
+@pytest.mark.parametrize("n,P", [(300, 2), (517, 3), (700, 4), (1090, 4), (1500, 8), (2049, 8)])
 def test_virtual_ranks_random_vs_oracle(sk, n, P):
     A = skewgen.random_skew(n, 5000 + n)
     nev = n // 2
@@ -109,7 +109,7 @@ def test_virtual_ranks_random_vs_oracle(sk, n, P):
     _check(A, lams, Zre, Zim, lam_o, Zre_o, Zim_o)
 
 
-@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("P", [2, 3, 8])
 def test_virtual_ranks_cluster_straddles_rank_boundary(sk, P):
     """A 100-fold repeated eigenvalue whose index range crosses the boundary between rank 0
     and rank 1 (ghost window + cluster rule of reading R9 across ranks)."""
