@@ -109,6 +109,30 @@ def test_config1_n4096_vs_oracle(sk):
     assert np.all(sin <= tol), f"max sin/tol {np.max(sin / tol):.3e}"
 
 
+@pytest.mark.parametrize("n,nev", [(12345, 6172), (9999, 700)])
+def test_odd_midsize_properties(sk, n, nev):
+    """Odd n with ragged tails in every kernel (last panel, last chase tasks, BT2 / BT1 strips,
+    the odd padding row of X), full and partial spectrum: every residual and every
+    orthogonality entry (sampled columns against all), the descending order, and for the full
+    half spectrum the Frobenius identity sum lam^2 = ||A||_F^2 / 2 (the zero eigenvalue of odd
+    n contributes nothing)."""
+    dev = torch.device("cuda", 0)
+    A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+    skewgen.random_skew_lower_device(A, n, n, torch.cuda.current_stream().cuda_stream)
+    S = torch.tril(A, -1)
+    S = S - S.t()
+    lam, Zre, Zim = sk.skew_eig(A, nev, overwrite_a=True)
+    del A
+    assert torch.all(lam[1:] <= lam[:-1]).item(), "descending"
+    assert lam[-1].item() > 0
+    res, orth, nA = _sampled_properties(S, lam, Zre, Zim, _sample_idx(nev))
+    assert res <= 1e-13, f"residual {res:.3e}"
+    assert orth <= 1e-11, f"orthogonality {orth:.3e}"
+    if nev == n // 2:
+        s2 = (lam * lam).sum().item()
+        assert abs(s2 - nA * nA / 2) <= 1e-12 * nA * nA
+
+
 def test_config3_n32768_sampled(sk):
     n = 32768
     nev = n // 2
