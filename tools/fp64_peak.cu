@@ -23,6 +23,15 @@ __global__ void dmma_loop(double* out, int iters){
   for(int i=0;i<CHAINS;i++) s+=c[i][0]+c[i][1];
   if(s==12345.678) out[0]=s;
 }
+// uniform [-1, 1) fill from a splitmix64 hash of the index (non-trivial operands: a zero-filled
+// DGEMM draws less power and can run faster than real data)
+__global__ void fill_random(double* p, size_t cnt, unsigned long long seed){
+  for(size_t i = blockIdx.x*(size_t)blockDim.x + threadIdx.x; i < cnt; i += (size_t)gridDim.x*blockDim.x){
+    unsigned long long z = seed*0x9E3779B97F4A7C15ull + i + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull; z = (z ^ (z >> 27)) * 0x94D049BB133111EBull; z ^= z >> 31;
+    p[i] = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+  }
+}
 template<int CHAINS>
 __global__ void dfma_loop(double* out, int iters){
   double c[CHAINS];
@@ -66,7 +75,7 @@ int main(){
   cublasHandle_t h; cublasCreate(&h);
   for(int n: {4096, 8192, 16384}){
     double *A,*B,*C; CK(cudaMalloc(&A,(size_t)n*n*8)); CK(cudaMalloc(&B,(size_t)n*n*8)); CK(cudaMalloc(&C,(size_t)n*n*8));
-    cudaMemset(A,0,(size_t)n*n*8); cudaMemset(B,0,(size_t)n*n*8);
+    fill_random<<<1024,256>>>(A,(size_t)n*n,1); fill_random<<<1024,256>>>(B,(size_t)n*n,2);
     double one=1, zero=0;
     cublasDgemm(h,CUBLAS_OP_N,CUBLAS_OP_N,n,n,n,&one,A,n,B,n,&zero,C,n);
     CK(cudaDeviceSynchronize());
