@@ -32,8 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "skew eig time-to-solution & FP64 TFLOP/s, n=32768 half spectrum, 1/2/4/8 B200"
-FP64_PEAK_TFLOPS = 37.13      # measured DMMA issue-rate peak on this pool (profiles/r01_fp64_peak.txt)
-FP64_DGEMM_TFLOPS = 35.71     # cuBLAS DGEMM 8192^3 sustained, same file (library ceiling, context)
+FP64_PEAK_TFLOPS = 37.13      # measured DMMA issue-rate peak on this pool (profiles/r02_fp64_peak.txt)
+FP64_DGEMM_TFLOPS = 35.75     # cuBLAS DGEMM 8192^3 sustained, random operands, same file (library ceiling, context)
 
 
 def parse():
@@ -273,7 +273,7 @@ def run_ours(args):
             traffic = None
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-            "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/r01_fp64_peak.txt); "
+            "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/r02_fp64_peak.txt); "
                            f"cuBLAS DGEMM sustained {FP64_DGEMM_TFLOPS} TF/s",
             "per_launch_flops": per_launch_flops, "per_launch_ms": per_launch_ms, "launches": dla}
     per_kernel = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
