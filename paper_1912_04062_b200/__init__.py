@@ -227,8 +227,13 @@ def _ctx(ctx):
 
 
 def _colmajor(torch, A):
-    """Column-major copy (as the transposed view of a contiguous tensor) of a 2-D tensor."""
-    return A.t().contiguous().t()
+    """Column-major COPY (the transposed view of a fresh contiguous tensor) of a 2-D tensor.
+    Always a copy: for an input that is already column-major, A.t().contiguous() would return
+    A's own storage and the solver (which destroys its input) would overwrite the caller's A
+    although overwrite_a=False."""
+    out = torch.empty((A.shape[1], A.shape[0]), dtype=A.dtype, device=A.device).t()
+    out.copy_(A)
+    return out
 
 
 def _new_colmajor(torch, n, m, device):

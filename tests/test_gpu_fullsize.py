@@ -160,6 +160,24 @@ def test_config3_n32768_sampled(sk):
     assert err <= 1e-12 * nA, f"max |lam - lam_oracle| = {err:.3e} = {err / nA:.2e} ||A||_F"
 
 
+def test_config3_eigvals_only_vs_golden(sk):
+    """BASELINE configs[3] through skew_eigvals (the eigenvalues-only path of configs[4]):
+    every eigenvalue against the oracle golden, and bit-identical to the eigenvalues of the
+    vector solve (the same bisection; tests above)."""
+    n = 32768
+    nev = n // 2
+    dev = torch.device("cuda", 0)
+    A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+    skewgen.random_skew_lower_device(A, n, n, torch.cuda.current_stream().cuda_stream)
+    nA = float(torch.linalg.norm(torch.tril(A, -1)).item()) * np.sqrt(2.0)
+    lam_v = sk.skew_eigvals(A, nev)          # copies A (overwrite_a=False)
+    lam, _, _ = sk.skew_eig(A, nev, overwrite_a=True)
+    assert torch.equal(lam_v, lam)
+    lam_o = _golden("eig_n32768_seed32768.txt")
+    err = np.max(np.abs(lam_v.cpu().numpy() - lam_o))
+    assert err <= 1e-12 * nA, f"max |lam - lam_oracle| = {err / nA:.2e} ||A||_F"
+
+
 def test_config2_bse_n10000_vs_oracle(sk):
     n = 10000
     h = n // 2

@@ -169,6 +169,29 @@ def test_pinned_host_output_overlap_matches_device(sk):
     _check_pairs(Afull, lam_h.numpy(), Zre_h.numpy(), Zim_h.numpy(), lam_o, Zre_o, Zim_o)
 
 
+def test_input_preserved_without_overwrite(sk):
+    """overwrite_a / overwrite_m = False leaves the caller's matrix untouched, for row-major
+    AND column-major inputs (a column-major tensor used to be passed through uncopied)."""
+    n = 300
+    A0 = torch.from_numpy(skewgen.random_skew(n, 41)).cuda()
+    for A in (A0.clone(), A0.t().contiguous().t().clone(memory_format=torch.preserve_format)):
+        Ac = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
+        Ac.copy_(A)
+        before = Ac.clone()
+        lam1 = sk.skew_eigvals(Ac)
+        assert torch.equal(Ac, before)
+        lam2, _, _ = sk.skew_eig(Ac)
+        assert torch.equal(Ac, before)
+        assert torch.equal(lam1, lam2)
+        sk.skew_eig_onestep(Ac)
+        assert torch.equal(Ac, before)
+    M = torch.empty((64, 64), dtype=torch.float64, device="cuda").t()
+    M.copy_(torch.from_numpy(skewgen.bse_spd(64, 3)))
+    Mb = M.clone()
+    sk.skew_eig_bse(M)
+    assert torch.equal(M, Mb)
+
+
 def test_bad_arguments(sk):
     import ctypes
     L = sk.lib()
