@@ -192,6 +192,33 @@ def test_input_preserved_without_overwrite(sk):
     assert torch.equal(M, Mb)
 
 
+@pytest.mark.parametrize("n,pad_a,pad_z", [(200, 3, 5), (257, 1, 0), (300, 0, 1), (1030, 7, 2)])
+def test_padded_leading_dimensions(sk, n, pad_a, pad_z):
+    """The C-ABI with lda = n + pad_a and ldz = n + pad_z (device buffers, odd or even, the
+    TMA paths' 16-byte stride rule not met for odd ones): the same eigenpairs as the oracle;
+    the padding rows of the outputs are not written."""
+    import ctypes
+    L = sk.lib()
+    ctx = sk.Context()
+    nev = n // 2
+    ctx.ensure_workspace(n, nev, sk.SKEW_WS_VECTORS)
+    A = skewgen.random_skew(n, 77 + n)
+    lda, ldz = n + pad_a, n + pad_z
+    Ab = torch.full((n, lda), 7.0, dtype=torch.float64, device="cuda")   # column j = row j of Ab
+    Ab[:, :n] = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    lam = torch.empty(nev, dtype=torch.float64, device="cuda")
+    Zre = torch.full((nev, ldz), 9.0, dtype=torch.float64, device="cuda")
+    Zim = torch.full((nev, ldz), 9.0, dtype=torch.float64, device="cuda")
+    rc = L.skew_eig(ctx.h, n, ctypes.c_void_p(Ab.data_ptr()), lda, nev, ctypes.c_void_p(lam.data_ptr()),
+                    ctypes.c_void_p(Zre.data_ptr()), ctypes.c_void_p(Zim.data_ptr()), ldz)
+    assert rc == 0, ctx.last_error()
+    if pad_z:
+        assert torch.all(Zre[:, n:] == 9.0) and torch.all(Zim[:, n:] == 9.0)
+    lam_o, Zre_o, Zim_o, _ = oracle.skew_eig(A, nev)
+    _check_pairs(A, lam.cpu().numpy(), Zre[:, :n].t().cpu().numpy(), Zim[:, :n].t().cpu().numpy(), lam_o,
+                 Zre_o, Zim_o)
+
+
 def test_bad_arguments(sk):
     import ctypes
     L = sk.lib()
