@@ -219,6 +219,25 @@ def test_padded_leading_dimensions(sk, n, pad_a, pad_z):
                  Zre_o, Zim_o)
 
 
+@pytest.mark.parametrize("k0,k1", [(0, 150), (37, 90), (100, 150), (149, 150)])
+def test_eig_range_single_context(sk, k0, k1):
+    """skew_eig_range on one (non-distributed) context: all eigenvalues, the vectors of
+    [k0, k1) only -- the ghost-window start is read back from the device bookkeeping when
+    k0 > 0 -- equal to the matching columns of the full solve's pairs (oracle-checked)."""
+    n = 300
+    A = skewgen.random_skew(n, 1234)
+    lam_o, Zre_o, Zim_o, _ = oracle.skew_eig(A)
+    lam, Zre, Zim = sk.skew_eig_range(_cuda(A), n // 2, k0, k1)
+    assert np.max(np.abs(lam.cpu().numpy() - lam_o)) <= 1e-12 * np.linalg.norm(A)
+    Z = Zre.cpu().numpy() + 1j * Zim.cpu().numpy()
+    Zo = Zre_o[:, k0:k1] + 1j * Zim_o[:, k0:k1]
+    lk = lam_o[k0:k1]
+    nA = np.linalg.norm(A)
+    assert np.max(np.linalg.norm(A @ Z - Z * (1j * lk), axis=0)) / (n * nA) <= 1e-13
+    assert np.max(np.abs(Z.conj().T @ Z - np.eye(k1 - k0))) <= 1e-11
+    assert np.max(np.abs(np.abs(np.sum(Zo.conj() * Z, axis=0)) - 1.0)) <= 1e-9   # simple spectrum
+
+
 def test_bad_arguments(sk):
     import ctypes
     L = sk.lib()
