@@ -238,6 +238,37 @@ def test_eig_range_single_context(sk, k0, k1):
     assert np.max(np.abs(np.abs(np.sum(Zo.conj() * Z, axis=0)) - 1.0)) <= 1e-9   # simple spectrum
 
 
+def test_concurrent_independent_contexts(sk):
+    """Distinct contexts are independent (include/skeweig.h): two contexts on two streams of
+    one device, driven by two host threads at once, each solve matches the oracle and its own
+    sequential result bit for bit."""
+    import threading
+    ns = (257, 400)
+    As = [skewgen.random_skew(n, 900 + n) for n in ns]
+    streams = [torch.cuda.Stream() for _ in ns]
+    ctxs = [sk.Context(stream=s) for s in streams]
+    ref = [sk.skew_eig(_cuda(A), ctx=c) for A, c in zip(As, ctxs)]
+    torch.cuda.synchronize()
+    out = [None, None]
+
+    def run(i):
+        with torch.cuda.stream(streams[i]):
+            for _ in range(3):
+                out[i] = sk.skew_eig(_cuda(As[i]), ctx=ctxs[i])
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    torch.cuda.synchronize()
+    for i, A in enumerate(As):
+        lam, Zre, Zim = out[i]
+        for x, y in zip(out[i], ref[i]):
+            assert torch.equal(x, y)
+        lam_o, Zre_o, Zim_o, _ = oracle.skew_eig(A)
+        _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
+
+
 def test_bad_arguments(sk):
     import ctypes
     L = sk.lib()
