@@ -159,6 +159,9 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if ws > 1 and rank != 0:
         return 0
+    # every host core (torchrun launches each rank with OMP_NUM_THREADS=1)
+    import oracle
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     n = args.n
     nev = args.nev or n // 2
     cpu_n = args.cpu_n

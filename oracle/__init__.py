@@ -60,6 +60,8 @@ def lib():
         L.orc_cholesky.restype = _c_i64
         L.orc_form_W.argtypes = [_c_i64, _c_dp, _c_i64, _c_dp, _c_i64]
         L.orc_num_threads.restype = ctypes.c_int
+        L.orc_set_num_threads.argtypes = [ctypes.c_int]
+        L.orc_set_num_threads.restype = None
         _lib = L
     return _lib
 
@@ -74,6 +76,11 @@ def _f(a):
 
 def num_threads():
     return lib().orc_num_threads()
+
+
+def set_num_threads(nt):
+    """Threads of the oracle's OpenMP loops (measurement harness only; no arithmetic)."""
+    lib().orc_set_num_threads(int(nt))
 
 
 def householder(x):

@@ -51,6 +51,16 @@ int orc_num_threads(void) {
 #endif
 }
 
+/* Thread count of the oracle's parallel loops (the reference arm under torchrun, whose
+   OMP_NUM_THREADS=1 default would otherwise time the oracle on one core).  No arithmetic. */
+void orc_set_num_threads(int nt) {
+#ifdef _OPENMP
+  if (nt > 0) omp_set_num_threads(nt);
+#else
+  (void)nt;
+#endif
+}
+
 /* ------------------------------------------------------------------------- */
 /* Householder reflector, LAPACK dlarfg convention (reading R3).
  * Given x (length m >= 1) returns v (v[0] = 1), tau, beta with
