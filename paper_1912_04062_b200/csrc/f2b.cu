@@ -434,14 +434,32 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
       if (lane == 0) { gmax = gm; bad = 0; }
     }
     __syncthreads();
-    // right-looking, one barrier per step: row k of R goes to Ms2 (Ms row k is read-only in
-    // step k), the trailing update uses R[k][r] R[k][c] = G'[k][r] G'[k][c] / d
-    for (int k = 0; k < KB; k++) {
-      const double d = Ms[k * LDK + k];
-      const double rkk = (d > 0.0) ? sqrt(d) : 1.0, inv = 1.0 / rkk;
-      if (tid == 0 && !(d > 1e-12 * gmax)) bad = 1;
-      if (tid >= k && tid < KB) Ms2[k * LDK + tid] = (tid == k) ? rkk : Ms[k * LDK + tid] * inv;
-      rank1_own(k, Ms + k * LDK, 1, inv * inv, Ms + k * LDK, true);
+    // right-looking, two columns and ONE barrier per step: rows k and k+1 of R go to Ms2 (Ms
+    // rows k, k+1 are read-only in the step; row k+1 is updated by column k on the fly), the
+    // trailing update uses R[k][r] R[k][c] + R[k+1][r] R[k+1][c]
+    static_assert(KB % 2 == 0, "two columns per step");
+    for (int k = 0; k < KB; k += 2) {
+      const double* g0 = Ms + k * LDK;            // G'[k][.]
+      const double* g1 = Ms + (k + 1) * LDK;      // G'[k+1][.] before column k's update
+      const double d0 = g0[k];
+      const double r0 = (d0 > 0.0) ? sqrt(d0) : 1.0, i0 = 1.0 / r0, s0 = i0 * i0;
+      const double x01 = g0[k + 1] * s0;          // column k's multiplier of row k+1
+      const double d1 = g1[k + 1] - x01 * g0[k + 1];
+      const double r1 = (d1 > 0.0) ? sqrt(d1) : 1.0, i1 = 1.0 / r1, s1 = i1 * i1;
+      if (tid == 0 && (!(d0 > 1e-12 * gmax) || !(d1 > 1e-12 * gmax))) bad = 1;
+      if (tid >= k && tid < KB) Ms2[k * LDK + tid] = (tid == k) ? r0 : g0[tid] * i0;
+      if (tid >= k + 1 && tid < KB) Ms2[(k + 1) * LDK + tid] = (tid == k + 1) ? r1 : (g1[tid] - x01 * g0[tid]) * i1;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int r = k + 2 + ti + 16 * u;
+        if (r >= KB) continue;
+        const double xa = g0[r] * s0, m1r = g1[r] - x01 * g0[r], xb = m1r * s1;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const int c = k + 2 + tj + 16 * v;
+          if (c < KB && c >= r) Ms[r * LDK + c] -= xa * g0[c] + xb * (g1[c] - x01 * g0[c]);
+        }
+      }
       __syncthreads();
     }
     for (int e = tid; e < KB * KB; e += blockDim.x) {
@@ -595,7 +613,9 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
     }
     __syncthreads();
     // T Y1^T = W column by column: T[:, c] = W[:, c] - sum_{l<c} T[:, l] Y1[c][l]; thread
-    // (row r, quarter q) sums l = q, q+4, ..; the 4 quarters combine with shuffles
+    // (row r, quarter q) sums l = q, q+4, ..; the 4 quarters combine with shuffles.  Row r
+    // only reads its own earlier entries (written by its quarter 0, same warp): a warp
+    // barrier per column, the rows run independently
     {
       const int r = tid >> 2, q = tid & 3;
       for (int c = 0; c < KB; c++) {
@@ -604,8 +624,9 @@ __global__ void __launch_bounds__(256, 1) panel_cqr_kernel(CqrArgs ca) {
         t += __shfl_xor_sync(0xffffffffu, t, 1);
         t += __shfl_xor_sync(0xffffffffu, t, 2);
         if (q == 0) Ts[r * LDK + c] = (c < r) ? 0.0 : ws[r * LDK + c] - t;
-        __syncthreads();
+        __syncwarp();
       }
+      __syncthreads();
     }
     {
       double v[NPT];   // gR row-major: element (r, c) at r * KB + c
