@@ -2,6 +2,7 @@
 // workspace planning, host/device staging, the stage driver of Algorithm 1 (ELPA2
 // flavour) and per-stage CUDA-event timing.  No compute happens on the host except
 // the small tridiagonal bookkeeping (split points, task lists) in tridiag.cu.
+#include <nvtx3/nvToolsExt.h>
 #include "../../include/skeweig.h"
 #include "../../include/skeweig_stages.h"
 #include "common.cuh"
@@ -143,6 +144,7 @@ struct skew_ctx_s {
   cudaEvent_t ev_start[ST_COUNT];
   cudaEvent_t ev_stop[ST_COUNT];
   bool used[ST_COUNT];
+  nvtxRangeId_t nvtx[ST_COUNT];   // host-side stage ranges for Nsight Systems (no-ops without a tool)
 };
 
 static int set_cuda_err(skew_ctx ctx, cudaError_t e, const char* where) {
@@ -156,8 +158,17 @@ static int set_cuda_err(skew_ctx ctx, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return set_cuda_err(ctx, _e, where); \
   } while (0)
 
-static void tstart(skew_ctx ctx, int s) { cudaEventRecord(ctx->ev_start[s], ctx->c.stream); ctx->used[s] = true; }
-static void tstop(skew_ctx ctx, int s) { cudaEventRecord(ctx->ev_stop[s], ctx->c.stream); }
+static const char* kStageNvtx[ST_COUNT] = {"skeweig full->band", "skeweig band->tridiagonal", "skeweig tridiagonal",
+                                           "skeweig BT2", "skeweig BT1", "skeweig output", "skeweig BSE"};
+static void tstart(skew_ctx ctx, int s) {
+  cudaEventRecord(ctx->ev_start[s], ctx->c.stream);
+  ctx->used[s] = true;
+  ctx->nvtx[s] = nvtxRangeStartA(kStageNvtx[s]);
+}
+static void tstop(skew_ctx ctx, int s) {
+  cudaEventRecord(ctx->ev_stop[s], ctx->c.stream);
+  nvtxRangeEnd(ctx->nvtx[s]);
+}
 static void tcollect(skew_ctx ctx) {
   for (int s = 0; s < ST_COUNT; s++) {
     float ms = 0.f;
