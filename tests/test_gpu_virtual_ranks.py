@@ -109,6 +109,17 @@ def test_virtual_ranks_random_vs_oracle(sk, n, P):
     _check(A, lams, Zre, Zim, lam_o, Zre_o, Zim_o)
 
 
+@pytest.mark.parametrize("n,nev,P", [(517, 100, 3), (1001, 37, 4), (700, 349, 8)])
+def test_virtual_ranks_partial_spectrum(sk, n, nev, P):
+    """Partial spectrum (nev < n/2) on P virtual ranks, odd n: ranges of unequal length, ghost
+    windows reaching across rank boundaries."""
+    A = skewgen.random_skew(n, 7000 + n)
+    lam_o, Zre_o, Zim_o, st = oracle.skew_eig(A, nev)
+    assert st == 0
+    lams, Zre, Zim = solve_virtual(sk, A, nev, P)
+    _check(A, lams, Zre, Zim, lam_o, Zre_o, Zim_o)
+
+
 @pytest.mark.parametrize("P", [2, 3, 8])
 def test_virtual_ranks_cluster_straddles_rank_boundary(sk, P):
     """A 100-fold repeated eigenvalue whose index range crosses the boundary between rank 0
