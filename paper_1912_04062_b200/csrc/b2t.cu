@@ -22,6 +22,7 @@
 #include "internal.h"
 #include <cooperative_groups.h>
 #include <vector>
+#include <type_traits>
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
@@ -343,22 +344,24 @@ __global__ void band_copy_kernel(const double* ABin, int64_t ldin, int64_t n, in
 // BT2 group prep: for group g (reflectors of sweeps s0..s0+K2-1 at chase position t) build
 // the dense staircase V (window rows rho = 0..RW-1 start at row s0 + t*b, reflector c at rows
 // rho = c+1 .. c+b), its forward compact-WY T (Q_g = I - V T V^T, dlarft from the Gram
-// matrix) and U = V T^T.  Stored per group as one contiguous block in exactly the shared-
-// memory layout of the apply kernel: [U (K2 x LDU) | -V (K2 x LDV)], U[c][rho], V[c][rho],
-// so that Q_g X = X + (-V) (U^T X) and one bulk copy moves the whole group.  The two row
+// matrix) and U = V T^T.  Stored per group: U (K2 x LDU), in the shared-memory layout of the
+// apply kernel, which places it beside -V (K2 x LDV) that its producer warps rebuild from the
+// reflectors (the staircase positions are fixed per group, the rest stays zero), so that
+// Q_g X = X + (-V) (U^T X) with one bulk copy per group and half the store.  The two row
 // strides differ (LDU = 4, LDV = 6 mod 16 doubles) because the apply kernel reads U with the
 // fragment pattern U[k0+t][c0+g] and V with V[r0+g][c0+2t+s]: both are then bank-conflict free.
 template <int K2, int RW>
 struct BT2Grp {
   static constexpr int LDU = RW + 4;
   static constexpr int LDV = RW + 6;
-  static constexpr int ELEMS = K2 * (LDU + LDV);
-  static_assert(LDU % 16 == 4 && LDV % 16 == 6 && (ELEMS % 2) == 0, "BT2 group layout");
+  static constexpr int ELEMS = K2 * (LDU + LDV);   // shared-memory block [U | -V]
+  static constexpr int UELEMS = K2 * LDU;           // stored per group: U
+  static_assert(LDU % 16 == 4 && LDV % 16 == 6 && (ELEMS % 2) == 0 && (UELEMS % 2) == 0, "BT2 group layout");
 };
 
 template <int K2, int RW>
 __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const double* qtau, int64_t ngroups, int b,
-                                                      double* UV) {
+                                                      double* UV, bool uonly) {
   using Gp = BT2Grp<K2, RW>;
   __shared__ double V[K2][RW];
   __shared__ double G[K2][K2 + 1];
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const d
       }
     }
     __syncthreads();
-    double* out = UV + g * Gp::ELEMS;
+    double* out = UV + g * (uonly ? Gp::UELEMS : Gp::ELEMS);
     for (int e = threadIdx.x; e < K2 * Gp::LDU; e += blockDim.x) {
       int c = e / Gp::LDU, rho = e % Gp::LDU;
       double u = 0.0;
@@ -399,10 +402,11 @@ __global__ void __launch_bounds__(128) bt2_prep_kernel(const double* qv, const d
         for (int c2 = c; c2 < K2; c2++) u += V[c2][rho] * T[c][c2];
       out[e] = u;
     }
-    for (int e = threadIdx.x; e < K2 * Gp::LDV; e += blockDim.x) {
-      int c = e / Gp::LDV, rho = e % Gp::LDV;
-      out[K2 * Gp::LDU + e] = (rho < RW) ? -V[c][rho] : 0.0;
-    }
+    if (!uonly)
+      for (int e = threadIdx.x; e < K2 * Gp::LDV; e += blockDim.x) {
+        int c = e / Gp::LDV, rho = e % Gp::LDV;
+        out[K2 * Gp::LDU + e] = (rho < RW) ? -V[c][rho] : 0.0;
+      }
     __syncthreads();
   }
 }
@@ -553,9 +557,10 @@ __device__ __forceinline__ void bt2_cw_gemm2(double* __restrict__ Xs, const doub
 // and signals mbarrier "full" (transaction bytes + cp.async completion arrivals).  The
 // ring offset advances by b per step inside a sweep block and by RW at a block boundary,
 // so the next block's first window never overlaps the window being computed.
-template <int NB, int K2, int RW, int RING, int BB, bool SPLIT>
+template <int NB, int K2, int RW, int RING, int BB, bool SPLIT, bool VQ>
 __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_ws_kernel(double* __restrict__ X, int64_t ldx, int64_t ncols, int64_t n,
-                                                       const double* __restrict__ UV, const int64_t* __restrict__ gofs,
+                                                       const double* __restrict__ UV, const double* __restrict__ qv,
+                                                       const int64_t* __restrict__ gofs,
                                                        int64_t nblk, long long* dbg, int nsplit_arg,
                                                        unsigned long long* prog) {
   using C = BT2Cfg<NB, K2, RW, RING, BB>;
@@ -578,8 +583,18 @@ __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_
   const int64_t blk0 = nblk - 1 - member;
   if (nblk <= 0 || blk0 < 0) return;
   for (int e = tid; e < C::XS; e += blockDim.x) Xs[e] = 0.0;   // ring rows beyond n stay finite
+  if (VQ) {
+    // -V outside the staircase: -0.0 inside the window rows, +0.0 in the pitch padding (the
+    // values the [U | -V] store carries, so both layouts give bit-identical products)
+    for (int e = tid; e < 2 * C::GS; e += blockDim.x) {
+      const int eb = e % C::GS - C::Gp::UELEMS;
+      G0[e] = (eb >= 0 && eb % C::LDV < RW) ? -0.0 : 0.0;
+    }
+  }
   if (tid == 0) {
-    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+    // full: the bulk copy's transaction count (+ the 4 producer warps' -V writes when the
+    // store holds U only)
+    mbar_init(&full[0], VQ ? 1 + C::NPW : 1); mbar_init(&full[1], VQ ? 1 + C::NPW : 1);
     mbar_init(&fullx[0], 128); mbar_init(&fullx[1], 128);
     mbar_init(&empty[0], C::NCW); mbar_init(&empty[1], C::NCW);
     mbar_fence_init();
@@ -632,12 +647,35 @@ __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_
         }
       }
     };
+    // the group's U by one bulk copy; its -V rebuilt by the producer warps from the reflectors
+    // (reflector c at window rows c+1 .. c+BB; the buffer is free: its step was released):
+    // the reflector loads are issued here, the shared-memory writes after the window-row loads
+    constexpr int PER = K2 * BB / (32 * C::NPW);   // 16 values per producer thread
+    static_assert(K2 * BB % (32 * C::NPW) == 0, "reflector block split");
+    double qvv[PER];
     auto load_group = [&](int64_t g, int b) {
+      constexpr int UE = VQ ? C::Gp::UELEMS : C::GS;   // U only, or the whole [U | -V] block
       if (ptid == 0) {
-        mbar_expect_tx(&full[b], (unsigned)(C::GS * sizeof(double)));
+        mbar_expect_tx(&full[b], (unsigned)(UE * sizeof(double)));
         fence_proxy_async();
-        bulk_g2s(G0 + b * C::GS, UV + g * C::GS, (unsigned)(C::GS * sizeof(double)), &full[b]);
+        bulk_g2s(G0 + b * C::GS, UV + g * UE, (unsigned)(UE * sizeof(double)), &full[b]);
       }
+      if (VQ) {
+        const double* qg = qv + g * K2 * BB;
+#pragma unroll
+        for (int i = 0; i < PER; i++) qvv[i] = __ldg(qg + ptid + 32 * C::NPW * i);
+      }
+    };
+    auto finish_group = [&](int b) {
+      if (!VQ) return;
+      double* Vs = G0 + b * C::GS + C::Gp::UELEMS;
+#pragma unroll
+      for (int i = 0; i < PER; i++) {
+        const int e = ptid + 32 * C::NPW * i, c = e / BB, d = e - c * BB;
+        Vs[c * C::LDV + c + 1 + d] = -qvv[i];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);
     };
     const int64_t pred = strip * nsplit + (member + nsplit - 1) % nsplit;
     auto wait_rows = [&](int64_t b, int64_t rend) {   // rows < rend of block b's input are final
@@ -665,6 +703,7 @@ __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_
     wait_rows(blk, blk * K2 + RW);
     load_rows(blk * K2, RW, 0);
     cp_async_mbar_arrive(&fullx[0]);
+    finish_group(0);
     int64_t pblk = -1, pt = 0;
     int poff = 0;
     bool pstored = true;    // step q-1 already written back
@@ -719,6 +758,7 @@ __global__ void __launch_bounds__(BT2Cfg<NB, K2, RW, RING, BB>::THREADS, 1) bt2_
           load_rows(nblk_ * K2, RW, noff);
         }
         cp_async_mbar_arrive(&fullx[b]);
+        finish_group(b);
         if (pub_blk >= 0) { publish(pub_blk, pub_rend); pub_blk = -1; }
       }
       pblk = blk; pt = t; poff = off; pstored = stored;
@@ -780,6 +820,8 @@ void B2TLayout::init(int64_t n_, int b_, int k2_) {
     g += 1 + (n - 3 - blk * k2) / b;
   }
   ngroups = g;
+  uonly = n > 40000;   // n = 65536: the [U | -V] store would be 54 GB per rank, U alone 27 GB
+  if (const char* v = getenv("SKEWEIG_BT2_UONLY")) uonly = atoi(v) != 0;   // experiments
 }
 
 cudaError_t band_extract(const double* A, int64_t lda, int64_t n, int b, double* AB, int64_t ldab, cudaStream_t st,
@@ -801,7 +843,8 @@ void b2t_reserve(Arena& ar, const B2TLayout& L, bool vectors, B2TWork& w) {
   int64_t ng = std::max<int64_t>(L.ngroups, 1);
   w.qv = ar.take<double>((size_t)ng * L.k2 * L.b);
   w.qtau = ar.take<double>((size_t)ng * L.k2);
-  if (vectors) w.qT = ar.take<double>((size_t)ng * L.k2 * (2 * (L.b + L.k2) + 10));   // [U | -V] per group (BT2Grp)
+  if (vectors)   // per group U (BT2Grp::UELEMS) or [U | -V] (BT2Grp::ELEMS)
+    w.qT = ar.take<double>((size_t)ng * L.k2 * (L.uonly ? (L.b + L.k2 + 4) : (2 * (L.b + L.k2) + 10)));
   w.gofs = ar.take<int64_t>(std::max<int64_t>(L.nblk, 1));
   if (vectors) w.prog = ar.take<unsigned long long>((size_t)4 * 2 * ((L.n + 63) / 64 + 1));   // BT2 wavefront flags
 }
@@ -862,7 +905,7 @@ cudaError_t bt2_prep(const B2TLayout& L, B2TWork& w, cudaStream_t st) {
   if (L.k2 != kBT2K2 || L.b != kBT2BB) return cudaErrorInvalidValue;
   KScope ks(KC_BT2_T, st);
   bt2_prep_kernel<kBT2K2, kBT2RW><<<(unsigned)std::min<int64_t>(L.ngroups, 8 * 148), 128, 0, st>>>(
-      w.qv, w.qtau, L.ngroups, kBT2BB, w.qT);
+      w.qv, w.qtau, L.ngroups, kBT2BB, w.qT, L.uonly);
   return cudaGetLastError();
 }
 
@@ -928,18 +971,25 @@ cudaError_t bt2_apply(const B2TLayout& L, B2TWork& w, double* X, int64_t ldx, in
       if (e2) return e2;
     }
     KScope ks(KC_BT2, st);
-    kern<<<(unsigned)grid, 32 * (NBv / 8 + 4), smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.gofs, L.nblk, dbgp,
+    kern<<<(unsigned)grid, 32 * (NBv / 8 + 4), smem, st>>>(X + cbeg * ldx, ldx, cnt, L.n, w.qT, w.qv, w.gofs, L.nblk, dbgp,
                                                            ns, w.prog);
     return cudaGetLastError();
   };
-  e = launch(bt2_ws_kernel<96, K2, RW, RING, BB, false>, BT2Cfg<96, K2, RW, RING, BB>::SMEM, 96, 0, c96, 1);
-  if (e) return e;
-  if (nsplit > 1)
-    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, true>, BT2Cfg<64, K2, RW, RING, BB>::SMEM, 64, c96, c64, nsplit);
-  else
-    e = launch(bt2_ws_kernel<64, K2, RW, RING, BB, false>, BT2Cfg<64, K2, RW, RING, BB>::SMEM, 64, c96, c64, 1);
-  if (e) return e;
-  e = launch(bt2_ws_kernel<32, K2, RW, RING, BB, false>, BT2Cfg<32, K2, RW, RING, BB>::SMEM, 32, c96 + c64, c32, 1);
+  auto launch_all = [&](auto vq) -> cudaError_t {
+    constexpr bool V = decltype(vq)::value;
+    cudaError_t e2 = launch(bt2_ws_kernel<96, K2, RW, RING, BB, false, V>, BT2Cfg<96, K2, RW, RING, BB>::SMEM, 96, 0,
+                            c96, 1);
+    if (e2) return e2;
+    if (nsplit > 1)
+      e2 = launch(bt2_ws_kernel<64, K2, RW, RING, BB, true, V>, BT2Cfg<64, K2, RW, RING, BB>::SMEM, 64, c96, c64,
+                  nsplit);
+    else
+      e2 = launch(bt2_ws_kernel<64, K2, RW, RING, BB, false, V>, BT2Cfg<64, K2, RW, RING, BB>::SMEM, 64, c96, c64, 1);
+    if (e2) return e2;
+    return launch(bt2_ws_kernel<32, K2, RW, RING, BB, false, V>, BT2Cfg<32, K2, RW, RING, BB>::SMEM, 32, c96 + c64,
+                  c32, 1);
+  };
+  e = L.uonly ? launch_all(std::true_type{}) : launch_all(std::false_type{});
   if (e) return e;
   return cudaGetLastError();
 }

@@ -152,6 +152,9 @@ struct B2TLayout {
   int64_t nblk = 0, ngroups = 0;
   std::vector<int64_t> gofs;   // first group index of each sweep block
   int64_t ldab = 0;
+  // BT2 group store: U only (the apply kernel rebuilds -V from the reflectors; half the
+  // store, ~4 % slower BT2) for large n, else [U | -V] with one bulk copy per group
+  bool uonly = false;
   void init(int64_t n_, int b_, int k2_);
 };
 

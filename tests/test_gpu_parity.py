@@ -269,6 +269,23 @@ def test_concurrent_independent_contexts(sk):
         _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
 
 
+@pytest.mark.parametrize("n", [1030, 2049])
+def test_bt2_u_only_store_bitwise(sk, n, monkeypatch):
+    """The BT2 group store holding U only (the apply kernel's producer warps rebuild -V from
+    the bulge reflectors; used for n > 40000, SKEWEIG_BT2_UONLY) gives bit-identical
+    eigenvectors to the [U | -V] store."""
+    A = skewgen.random_skew(n, 4321 + n)
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("SKEWEIG_BT2_UONLY", v)
+        out.append(sk.skew_eig(_cuda(A), ctx=sk.Context()))
+    for x, y in zip(*out):
+        assert torch.equal(x, y)
+    lam_o, Zre_o, Zim_o, _ = oracle.skew_eig(A)
+    lam, Zre, Zim = out[1]
+    _check_pairs(A, lam.cpu().numpy(), Zre.cpu().numpy(), Zim.cpu().numpy(), lam_o, Zre_o, Zim_o)
+
+
 def test_bad_arguments(sk):
     import ctypes
     L = sk.lib()
