@@ -7,6 +7,7 @@
 // NotDefinite when a pivot <= n*eps*max_i M_ii (reading R18).
 #include "common.cuh"
 #include "gemm_dmma.cuh"
+#include "tma_gemm.cuh"
 #include "internal.h"
 #include <algorithm>
 #include <cfloat>
@@ -107,6 +108,15 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
   cudaError_t e;
   const int64_t nbl = (n + kCholNB - 1) / kCholNB;
   KScope ks(KC_BSE, st, (int)(1 + nbl + 2 * (nbl - 1) + 4));
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // the TMA-fed persistent GEMM where the strides allow it (16-byte rows), else the cp.async one
+  auto gemm_tn = [&](const GemmArgs& ga) -> cudaError_t {   // C = alpha A^T B
+    cudaError_t r = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 16, 6, true, false, false, false>(ga, nsm, st);
+    if (r == cudaErrorNotSupported) r = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
+    return r;
+  };
   cudaMemsetAsync(status_d, 0, sizeof(int64_t), st);
   diag_max_kernel<<<1, 256, 0, st>>>(M, ldm, n, scratch);
   for (int64_t j0 = 0; j0 < n; j0 += kCholNB) {
@@ -120,7 +130,8 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
       const double* L21 = M + SK_IDX(j0 + nb, j0, ldm);
       ga.A = L21; ga.lda = ldm; ga.B = L21; ga.ldb = ldm;
       ga.C = M + SK_IDX(j0 + nb, j0 + nb, ldm); ga.ldc = ldm; ga.alpha = -1.0; ga.beta = 1.0; ga.tri_off = 0;
-      e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
+      e = tma_disabled() ? cudaErrorNotSupported : tma_gemm<128, 64, 32, 3, false, true, true, true>(ga, nsm, st);
+      if (e == cudaErrorNotSupported) e = gemm_dmma<64, 64, 16, 32, 32, 2, false, true, true>(ga, st);
       if (e) return e;
     }
   }
@@ -134,7 +145,7 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
     GemmArgs ga;
     ga.M = m; ga.N = m; ga.K = m;
     ga.A = M; ga.lda = ldm; ga.B = M + m; ga.ldb = ldm; ga.C = S; ga.ldc = lds; ga.alpha = 1.0; ga.beta = 0.0;
-    e = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
+    e = gemm_tn(ga);
     if (e) return e;
   }
   // W21 = -L22^T L11
@@ -143,7 +154,7 @@ cudaError_t bse_front(double* M, int64_t ldm, int64_t n, double* W, int64_t ldw,
     ga.M = m; ga.N = m; ga.K = m;
     ga.A = M + SK_IDX(m, m, ldm); ga.lda = ldm; ga.B = M; ga.ldb = ldm; ga.C = W + m; ga.ldc = ldw;
     ga.alpha = -1.0; ga.beta = 0.0;
-    e = gemm_dmma<64, 64, 16, 32, 32, 2, true, false, false>(ga, st);
+    e = gemm_tn(ga);
     if (e) return e;
   }
   {
